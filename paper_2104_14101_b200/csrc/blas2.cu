@@ -1,0 +1,110 @@
+// Matrix-vector kernels for the preconditioner solves (preconditioner.py:42-53):
+// row GEMV with triangular bounds (explicit L^-1 and L^-T applies replace the
+// two LAPACK trsv calls of tri_solve, linalg.py:47-55) and the deterministic
+// column GEMV (SA^T u) used by the Woodbury path.  Vectors are fp64; matrix
+// elements are T.  No atomics.
+#include "blas2.cuh"
+#include "common.cuh"
+
+namespace adask {
+
+// out[i] = alpha * sum_{j in J(i)} M[i*ld + j] * x[j]   (+ beta_vec? handled by caller)
+// mode 0: J = [0, cols), 1: J = [0, i] (lower), 2: J = [i, cols) (upper)
+template <typename T>
+__global__ void __launch_bounds__(256) k_gemv_rows(const T* __restrict__ M, int64_t rows,
+                                                   int64_t cols, int64_t ld,
+                                                   const double* __restrict__ x, double alpha,
+                                                   double* __restrict__ out, int mode) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= rows) return;
+  int64_t j0 = 0, j1 = cols;
+  if (mode == 1) j1 = i + 1 < cols ? i + 1 : cols;
+  if (mode == 2) j0 = i;
+  const T* r = M + i * ld;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t j = j0 + lane;
+  for (; j + 96 < j1; j += 128) {
+    s0 = fma((double)r[j], x[j], s0);
+    s1 = fma((double)r[j + 32], x[j + 32], s1);
+    s2 = fma((double)r[j + 64], x[j + 64], s2);
+    s3 = fma((double)r[j + 96], x[j + 96], s3);
+  }
+  for (; j < j1; j += 32) s0 = fma((double)r[j], x[j], s0);
+  double s = (s0 + s1) + (s2 + s3);
+  s = warp_sum(s);
+  if (lane == 0) out[i] = alpha * s;
+}
+
+// part[b][j] = sum_{i in rows of chunk b} M[i*ld + j] * u[i]
+template <typename T>
+__global__ void k_gemv_cols(const T* __restrict__ M, int64_t rows, int64_t cols, int64_t ld,
+                            const double* __restrict__ u, double* __restrict__ part) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nb = gridDim.y;
+  const int64_t r0 = rows * blockIdx.y / nb, r1 = rows * (blockIdx.y + 1) / nb;
+  if (j >= cols) return;
+  double s = 0.0;
+  for (int64_t i = r0; i < r1; ++i) s = fma(u[i], (double)M[i * ld + j], s);
+  part[(int64_t)blockIdx.y * cols + j] = s;
+}
+
+// Woodbury epilogue: out = (y - (sum_b part[b]) / lam) / nu2   (y = z / lam)
+__global__ void k_woodbury_finish(const double* __restrict__ part, int nb, int64_t d,
+                                  const double* __restrict__ y, const double* __restrict__ lam,
+                                  double nu2, double* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * d + j];
+  out[j] = (y[j] - s / lam[j]) / nu2;
+}
+
+__global__ void k_div_vec(const double* __restrict__ z, const double* __restrict__ lam, int64_t d,
+                          double* __restrict__ y) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < d) y[j] = z[j] / lam[j];
+}
+
+int gemv_rows(adask_ctx* ctx, int dtype, const void* M, int64_t rows, int64_t cols, int64_t ld,
+              const double* x, double alpha, double* out, int mode, cudaStream_t st) {
+  if (rows <= 0) return ADASK_OK;
+  const unsigned blocks = (unsigned)cdiv(rows * 32, 256);
+  if (dtype == ADASK_F64)
+    k_gemv_rows<double><<<blocks, 256, 0, st>>>((const double*)M, rows, cols, ld, x, alpha, out, mode);
+  else
+    k_gemv_rows<float><<<blocks, 256, 0, st>>>((const float*)M, rows, cols, ld, x, alpha, out, mode);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
+int woodbury_apply(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t d, int64_t ldsa,
+                   const void* Linv, const void* LinvT, int64_t ldl, const double* lam, double nu2,
+                   const double* z, double* out, cudaStream_t st) {
+  // scratch: y (d), w (m), t (m), u (m), partials (nb * d)
+  const int nb = (int)std::min<int64_t>(std::max<int64_t>(1, m / 16), 64);
+  const size_t a = 256;
+  size_t off_w = align_up((size_t)d * 8, a), off_t = off_w + align_up((size_t)m * 8, a);
+  size_t off_u = off_t + align_up((size_t)m * 8, a), off_p = off_u + align_up((size_t)m * 8, a);
+  void* wsp = nullptr;
+  ADASK_TRY(ctx->ws[WS_GEMV].get(off_p + (size_t)nb * d * 8, st, &wsp));
+  char* b = (char*)wsp;
+  double *y = (double*)b, *w = (double*)(b + off_w), *t = (double*)(b + off_t);
+  double *u = (double*)(b + off_u), *part = (double*)(b + off_p);
+  k_div_vec<<<(unsigned)cdiv(d, 256), 256, 0, st>>>(z, lam, d, y);
+  ADASK_LAUNCHED(ctx);
+  ADASK_TRY(gemv_rows(ctx, dtype, SA, m, d, ldsa, y, 1.0, w, 0, st));     // w = SA y
+  ADASK_TRY(gemv_rows(ctx, dtype, Linv, m, m, ldl, w, 1.0, t, 1, st));    // t = L^-1 w
+  ADASK_TRY(gemv_rows(ctx, dtype, LinvT, m, m, ldl, t, 1.0, u, 2, st));   // u = L^-T t
+  dim3 g((unsigned)cdiv(d, 256), (unsigned)nb);
+  if (dtype == ADASK_F64)
+    k_gemv_cols<double><<<g, 256, 0, st>>>((const double*)SA, m, d, ldsa, u, part);
+  else
+    k_gemv_cols<float><<<g, 256, 0, st>>>((const float*)SA, m, d, ldsa, u, part);
+  ADASK_LAUNCHED(ctx);
+  k_woodbury_finish<<<(unsigned)cdiv(d, 256), 256, 0, st>>>(part, nb, d, y, lam, nu2, out);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
+}  // namespace adask

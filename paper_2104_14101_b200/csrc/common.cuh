@@ -1,0 +1,136 @@
+// Shared plumbing for libadask: status handling, the device context and its
+// grow-only workspaces, launch accounting, small device helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/adask.h"
+
+namespace adask {
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
+void set_error(const char* fmt, ...);
+int fail(int status, const char* fmt, ...);
+
+#define ADASK_CUDA(expr)                                                              \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return ::adask::fail(ADASK_E_CUDA, "%s failed: %s (%s:%d)", #expr,              \
+                           cudaGetErrorString(_e), __FILE__, __LINE__);               \
+  } while (0)
+
+#define ADASK_TRY(expr)          \
+  do {                           \
+    int _s = (expr);             \
+    if (_s != ADASK_OK) return _s; \
+  } while (0)
+
+#define ADASK_LAUNCHED(ctx)                                                            \
+  do {                                                                                 \
+    cudaError_t _e = cudaGetLastError();                                               \
+    if (_e != cudaSuccess)                                                             \
+      return ::adask::fail(ADASK_E_CUDA, "kernel launch failed: %s (%s:%d)",           \
+                           cudaGetErrorString(_e), __FILE__, __LINE__);                \
+    (ctx)->launches++;                                                                 \
+  } while (0)
+
+// Grow-only device scratch buffer.  Growth synchronises the stream first so a
+// buffer still in use by queued kernels is never freed under them.
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int get(size_t need, cudaStream_t st, void** out) {
+    if (need > bytes) {
+      if (ptr) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail(ADASK_E_CUDA, "sync: %s", cudaGetErrorString(e));
+        cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+      }
+      size_t nb = need + need / 4 + 4096;
+      cudaError_t e = cudaMalloc(&ptr, nb);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ADASK_E_NOMEM, "cudaMalloc(%zu) failed: %s", nb, cudaGetErrorString(e));
+      }
+      bytes = nb;
+    }
+    *out = ptr;
+    return ADASK_OK;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+enum WsSlot {
+  WS_HESS = 0,   // hess_mult per-CTA partial d-vectors
+  WS_RNG,        // sign / bucket streams, rejection lists
+  WS_SORT,       // SJLT counting-sort keys / values / CUB temp
+  WS_SRHT,       // pruned FWHT intermediate
+  WS_GAUSS,      // Gaussian S tiles
+  WS_CHOL,       // factorization scratch
+  WS_VEC,        // iteration-body scratch (scalars, temporaries)
+  WS_SMALL,      // small host-visible-by-copy scalars
+  WS_SIGNS,      // SRHT sign stream
+  WS_PLAN,       // SRHT slot / entry plan
+  WS_GEMM,       // split-K partials of gemm_impl
+  WS_GEMV,       // partials of column GEMVs (precond apply)
+  WS_GRAM,       // Gram / capacitance matrix being factored
+  WS_APPLY,      // temporaries of the dense preconditioner apply
+  WS_COUNT
+};
+
+}  // namespace adask
+
+struct adask_ctx {
+  int device = 0;
+  int64_t launches = 0;
+  adask::Workspace ws[adask::WS_COUNT];
+  double* pinned = nullptr;  // pinned host scalars for synchronous readbacks
+  int* pinned_flags = nullptr;
+};
+
+namespace adask {
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Activate ctx's device for the calling thread.
+int use_device(adask_ctx* ctx);
+
+// ---------------------------------------------------------------- device utils
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction of one double (fixed tree, any blockDim that is
+// a multiple of 32, <= 1024).  All threads get the result.
+__device__ __forceinline__ double block_sum(double v, double* sh /*[32]*/) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = (lane < nw) ? sh[lane] : 0.0;
+  t = warp_sum(t);
+  return t;
+}
+
+}  // namespace adask

@@ -1,0 +1,63 @@
+// Gaussian sketch SA = S A, S = N(0, 1/m)          reference: embeddings.py:66-73
+//
+// S[k, i] = Philox4x32-10 / Box-Muller normal (rng.cuh) divided by sqrt(m),
+// keyed by the sketch seed and indexed by (sketch row k, GLOBAL row i of A),
+// so a row-sharded A gives per-shard partial sketches that sum to the full
+// one.  This fp64/fp32 path generates S in column chunks into HBM and runs the
+// FP64/FP32-pipe GEMM (gemm.cu); the TF32 tensor-core path with S generated
+// on the fly in shared memory is gauss_tc.cu (ADASK_TF32).
+#include "common.cuh"
+#include "gemm.cuh"
+#include "rng.cuh"
+
+namespace adask {
+
+int gauss_tc_impl(adask_ctx* ctx, const float* A, int64_t n_local, int64_t d, int64_t lda,
+                  int64_t row0, int64_t m, uint64_t key, float* SA, int64_t ldsa, bool accumulate,
+                  cudaStream_t st);
+
+}  // namespace adask
+
+using namespace adask;
+
+extern "C" int adask_sketch_gaussian(adask_ctx* ctx, int dtype, const void* A, int64_t n_local,
+                                     int64_t d, int64_t lda, int64_t row0, int64_t m, uint64_t key,
+                                     void* SA, int64_t ldsa, uint32_t flags, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (m < 1) return fail(ADASK_E_SKETCH_TOO_LARGE, "sketch size must be a positive integer, got %lld",
+                         (long long)m);
+  if (n_local < 0 || d < 1 || lda < d || ldsa < d || row0 < 0)
+    return fail(ADASK_E_DIM, "sketch_gaussian: bad shape");
+  if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
+  cudaStream_t st = S(stream);
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  const bool accumulate = (flags & ADASK_ACCUMULATE) != 0;
+  if ((flags & ADASK_TF32) && dtype == ADASK_F32) {
+    return gauss_tc_impl(ctx, (const float*)A, n_local, d, lda, row0, m, key, (float*)SA, ldsa,
+                         accumulate, st);
+  }
+  if (n_local == 0) {
+    if (!accumulate) ADASK_CUDA(cudaMemset2DAsync(SA, ldsa * esz, 0, d * esz, m, st));
+    return ADASK_OK;
+  }
+  // chunk of S columns (rows of A) so that S_chunk stays <= 256 MiB
+  int64_t nc = (int64_t)((256ll << 20) / ((int64_t)m * (int64_t)esz));
+  nc = std::max<int64_t>(256, nc / 256 * 256);
+  nc = std::min<int64_t>(nc, n_local);
+  void* wsp = nullptr;
+  ADASK_TRY(ctx->ws[WS_GAUSS].get((size_t)m * nc * esz, st, &wsp));
+  const double sc = sqrt((double)m);
+  const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+  for (int64_t c0 = 0; c0 < n_local; c0 += nc) {
+    const int64_t w = std::min<int64_t>(nc, n_local - c0);
+    ADASK_TRY(adask_philox_gaussian(ctx, dtype, m, row0 + c0, w, key, wsp, w, stream));
+    const void* Ac = (const char*)A + (size_t)c0 * lda * esz;
+    const double beta = (c0 > 0 || accumulate) ? 1.0 : 0.0;
+    ADASK_TRY(gemm_impl(ctx, dtype, m, d, w, 1.0, wsp, w, false, Ac, lda, false, nullptr, beta, SA,
+                        ldsa, 0.0, nullptr, false, st));
+  }
+  (void)sc;
+  (void)k0;
+  (void)k1;
+  return ADASK_OK;
+}

@@ -1,0 +1,286 @@
+// Fused iteration bodies of the sketched solvers.
+// reference: solvers.py:227-282 (_PcgState), :522-571 (_IhsState, _PolyakState).
+//
+// Each body is: one fused A^T A pass (hessmult.cu), one single-CTA d-vector
+// kernel (dots, step sizes, axpys, guards), one preconditioner apply, one
+// single-CTA reduction kernel, and one 64-byte device->host readback of the
+// decrement plus guard flags -- the single host synchronisation the adaptive
+// accept/reject rule needs per loop pass.  All reductions are fixed-order
+// (bitwise reproducible).
+#include "common.cuh"
+#include "hessmult.cuh"
+#include "precond.cuh"
+
+namespace adask {
+
+enum { FLAG_NEGATIVE = 1, FLAG_BREAKDOWN = 2 };
+
+struct IterScalars {
+  double delta_tilde;
+  double pad[3];
+  int flags;
+  int pad2[7];
+};
+
+constexpr int kVecThreads = 1024;
+
+// Fixed-order block sum (kVecThreads threads).
+__device__ __forceinline__ double blk_sum(double v, double* sh) { return block_sum(v, sh); }
+
+// PCG restart tail: r = -g (g = H x - B); p = rt; dt_col = max(colsum(r*rt),0)
+// with the NegativeValue guard (solvers.py:245-255).
+__global__ void __launch_bounds__(kVecThreads) k_pcg_restart_tail(int64_t d, int64_t c, const double* rt,
+                                                                  double* r, double* p, double* dt_col,
+                                                                  IterScalars* sc) {
+  __shared__ double sh[32];
+  double tot = 0.0;
+  int flags = 0;
+  for (int64_t j = 0; j < c; ++j) {
+    double s = 0.0, q = 0.0;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+      double rv = r[j * d + i];
+      double tv = rt[j * d + i];
+      s = fma(rv, tv, s);
+      q = fma(rv, rv, q);
+      p[j * d + i] = tv;
+    }
+    s = blk_sum(s, sh);
+    q = blk_sum(q, sh);
+    if (s < -1e-12 * q) flags |= FLAG_NEGATIVE;
+    double dt = s > 0.0 ? s : 0.0;
+    if (threadIdx.x == 0) dt_col[j] = dt;
+    tot += dt;
+  }
+  if (threadIdx.x == 0) {
+    sc->delta_tilde = 0.5 * tot;
+    sc->flags = flags;
+  }
+}
+
+__global__ void k_negate(double* v, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = -v[i];
+}
+
+// PCG propose, first half (solvers.py:265-272)
+__global__ void __launch_bounds__(kVecThreads) k_pcg_step(int64_t d, int64_t c, const double* x,
+                                                          const double* r, const double* p,
+                                                          const double* Hp, const double* dt_col,
+                                                          double* x_new, double* r_new,
+                                                          IterScalars* sc) {
+  __shared__ double sh[32];
+  int flags = 0;
+  for (int64_t j = 0; j < c; ++j) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s = fma(p[j * d + i], Hp[j * d + i], s);
+    const double pHp = blk_sum(s, sh);
+    const bool active = dt_col[j] > 0.0;
+    if (active && pHp <= 0.0) flags |= FLAG_BREAKDOWN;
+    const double alpha = active ? dt_col[j] / (pHp > 0.0 ? pHp : 1.0) : 0.0;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+      x_new[j * d + i] = x[j * d + i] + p[j * d + i] * alpha;
+      r_new[j * d + i] = r[j * d + i] - Hp[j * d + i] * alpha;
+    }
+  }
+  if (threadIdx.x == 0) sc->flags = flags;
+}
+
+// PCG propose, second half: dt_new = _scalars(r_new, rt_new)
+__global__ void __launch_bounds__(kVecThreads) k_pcg_scalars(int64_t d, int64_t c, const double* r,
+                                                             const double* rt, double* dt_new,
+                                                             IterScalars* sc) {
+  __shared__ double sh[32];
+  double tot = 0.0;
+  int flags = 0;
+  for (int64_t j = 0; j < c; ++j) {
+    double s = 0.0, q = 0.0;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+      double rv = r[j * d + i];
+      s = fma(rv, rt[j * d + i], s);
+      q = fma(rv, rv, q);
+    }
+    s = blk_sum(s, sh);
+    q = blk_sum(q, sh);
+    if (s < -1e-12 * q) flags |= FLAG_NEGATIVE;
+    double dt = s > 0.0 ? s : 0.0;
+    if (threadIdx.x == 0) dt_new[j] = dt;
+    tot += dt;
+  }
+  if (threadIdx.x == 0) {
+    sc->delta_tilde = 0.5 * tot;
+    sc->flags |= flags;
+  }
+}
+
+// commit: p = rt_new + p * ratio,  ratio = old > 0 ? dt_new / old : 0  (solvers.py:277-282)
+__global__ void k_pcg_commit(int64_t d, int64_t c, const double* rt_new, const double* dt_new,
+                             const double* dt_old, double* p) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d * c) return;
+  const int64_t j = i / d;
+  const double old = dt_old[j];
+  const double ratio = old > 0.0 ? dt_new[j] / old : 0.0;
+  p[i] = rt_new[i] + p[i] * ratio;
+}
+
+// 0.5 * sum(a .* b)
+__global__ void __launch_bounds__(kVecThreads) k_half_dot(int64_t d, int64_t c, int64_t ld,
+                                                          const double* a, const double* b,
+                                                          IterScalars* sc) {
+  __shared__ double sh[32];
+  double tot = 0.0;
+  for (int64_t j = 0; j < c; ++j) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s = fma(a[j * ld + i], b[j * ld + i], s);
+    tot += blk_sum(s, sh);
+  }
+  if (threadIdx.x == 0) {
+    sc->delta_tilde = 0.5 * tot;
+    sc->flags = 0;
+  }
+}
+
+// IHS / heavy-ball step: x_new = x - mu v (+ beta (x - x_prev))   (solvers.py:538, 562)
+__global__ void k_ihs_step(int64_t n, const double* x, const double* v, double mu,
+                           const double* x_prev, double beta, double* x_new) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double t = x[i] - mu * v[i];
+  if (x_prev) t = t + beta * (x[i] - x_prev[i]);
+  x_new[i] = t;
+}
+
+static int get_scalars(adask_ctx* ctx, IterScalars** sc, cudaStream_t st) {
+  void* wsp = nullptr;
+  ADASK_TRY(ctx->ws[WS_SMALL].get(sizeof(IterScalars), st, &wsp));
+  *sc = (IterScalars*)wsp;
+  return ADASK_OK;
+}
+
+static int read_scalars(adask_ctx* ctx, IterScalars* sc, double* dt_host, int* flags,
+                        cudaStream_t st) {
+  ADASK_CUDA(cudaMemcpyAsync(ctx->pinned, sc, sizeof(IterScalars), cudaMemcpyDeviceToHost, st));
+  ADASK_CUDA(cudaStreamSynchronize(st));
+  const IterScalars* h = reinterpret_cast<const IterScalars*>(ctx->pinned);
+  if (dt_host) *dt_host = h->delta_tilde;
+  *flags = h->flags;
+  return ADASK_OK;
+}
+
+static int check_problem(const adask_problem* pb) {
+  if (!pb || !pb->A || pb->n < 0 || pb->d < 1 || pb->c < 1 || pb->lda < pb->d || !pb->lam)
+    return fail(ADASK_E_ARG, "bad problem descriptor");
+  return ADASK_OK;
+}
+
+}  // namespace adask
+
+using namespace adask;
+
+extern "C" int adask_pcg_restart(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P,
+                                 const double* x, double* r, double* rt, double* p, double* dt_col,
+                                 double* delta_tilde_host, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  ADASK_TRY(check_problem(pb));
+  cudaStream_t st = S(stream);
+  const int64_t d = pb->d, c = pb->c;
+  // r = B - H x   (computed as -(H x - B), exact)
+  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, x, c, d, pb->nu2, pb->lam, pb->B,
+                           d, r, d, 0, st));
+  k_negate<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(r, d * c);
+  ADASK_LAUNCHED(ctx);
+  ADASK_TRY(precond_apply_impl(ctx, P, r, c, d, rt, d, st));
+  IterScalars* sc = nullptr;
+  ADASK_TRY(get_scalars(ctx, &sc, st));
+  k_pcg_restart_tail<<<1, kVecThreads, 0, st>>>(d, c, rt, r, p, dt_col, sc);
+  ADASK_LAUNCHED(ctx);
+  int flags = 0;
+  ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
+  if (flags & FLAG_NEGATIVE) return fail(ADASK_E_NEGATIVE, "r.T H_S^-1 r went negative beyond roundoff");
+  return ADASK_OK;
+}
+
+extern "C" int adask_pcg_propose(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P,
+                                 const double* x, const double* r, const double* p,
+                                 const double* dt_col, double* Hp, double* x_new, double* r_new,
+                                 double* rt_new, double* dt_new, double* delta_tilde_host,
+                                 void* stream) {
+  ADASK_TRY(use_device(ctx));
+  ADASK_TRY(check_problem(pb));
+  cudaStream_t st = S(stream);
+  const int64_t d = pb->d, c = pb->c;
+  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, c, d, pb->nu2, pb->lam,
+                           nullptr, d, Hp, d, 0, st));
+  IterScalars* sc = nullptr;
+  ADASK_TRY(get_scalars(ctx, &sc, st));
+  k_pcg_step<<<1, kVecThreads, 0, st>>>(d, c, x, r, p, Hp, dt_col, x_new, r_new, sc);
+  ADASK_LAUNCHED(ctx);
+  ADASK_TRY(precond_apply_impl(ctx, P, r_new, c, d, rt_new, d, st));
+  k_pcg_scalars<<<1, kVecThreads, 0, st>>>(d, c, r_new, rt_new, dt_new, sc);
+  ADASK_LAUNCHED(ctx);
+  int flags = 0;
+  ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
+  if (flags & FLAG_BREAKDOWN) return fail(ADASK_E_BREAKDOWN, "direction with nonpositive curvature");
+  if (flags & FLAG_NEGATIVE) return fail(ADASK_E_NEGATIVE, "r.T H_S^-1 r went negative beyond roundoff");
+  return ADASK_OK;
+}
+
+extern "C" int adask_pcg_commit(adask_ctx* ctx, int64_t d, int64_t c, const double* rt_new,
+                                const double* dt_new, const double* dt_old, double* p, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  cudaStream_t st = S(stream);
+  k_pcg_commit<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(d, c, rt_new, dt_new, dt_old, p);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
+extern "C" int adask_ihs_restart(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P,
+                                 const double* x, double* g, double* v, double* delta_tilde_host,
+                                 void* stream) {
+  ADASK_TRY(use_device(ctx));
+  ADASK_TRY(check_problem(pb));
+  cudaStream_t st = S(stream);
+  const int64_t d = pb->d, c = pb->c;
+  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, x, c, d, pb->nu2, pb->lam, pb->B,
+                           d, g, d, 0, st));
+  ADASK_TRY(precond_apply_impl(ctx, P, g, c, d, v, d, st));
+  IterScalars* sc = nullptr;
+  ADASK_TRY(get_scalars(ctx, &sc, st));
+  k_half_dot<<<1, kVecThreads, 0, st>>>(d, c, d, g, v, sc);
+  ADASK_LAUNCHED(ctx);
+  int flags = 0;
+  return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
+}
+
+extern "C" int adask_ihs_propose(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P,
+                                 const double* x, const double* v, double mu, const double* x_prev,
+                                 double beta, double* x_new, double* g_new, double* v_new,
+                                 double* delta_tilde_host, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  ADASK_TRY(check_problem(pb));
+  cudaStream_t st = S(stream);
+  const int64_t d = pb->d, c = pb->c;
+  k_ihs_step<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(d * c, x, v, mu, x_prev, beta, x_new);
+  ADASK_LAUNCHED(ctx);
+  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, x_new, c, d, pb->nu2, pb->lam,
+                           pb->B, d, g_new, d, 0, st));
+  ADASK_TRY(precond_apply_impl(ctx, P, g_new, c, d, v_new, d, st));
+  IterScalars* sc = nullptr;
+  ADASK_TRY(get_scalars(ctx, &sc, st));
+  k_half_dot<<<1, kVecThreads, 0, st>>>(d, c, d, g_new, v_new, sc);
+  ADASK_LAUNCHED(ctx);
+  int flags = 0;
+  return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
+}
+
+extern "C" int adask_dot(adask_ctx* ctx, const double* a, const double* b, int64_t d, int64_t c,
+                         int64_t ld, double* result_host, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  cudaStream_t st = S(stream);
+  IterScalars* sc = nullptr;
+  ADASK_TRY(get_scalars(ctx, &sc, st));
+  k_half_dot<<<1, kVecThreads, 0, st>>>(d, c, ld, a, b, sc);
+  ADASK_LAUNCHED(ctx);
+  int flags = 0;
+  return read_scalars(ctx, sc, result_host, &flags, st);
+}

@@ -1,0 +1,191 @@
+// Sketched-Hessian preconditioner H_S = SA^T SA + nu^2 Lam.
+// reference: preconditioner.py:26-74 (Preconditioner, build, solve).
+//
+// build: m >= d (ties dense, :63) -> Gram H_S (d x d) on the lower triangle
+//        with nu^2 lam folded into the GEMM epilogue, then Cholesky + L^-1;
+//        m <  d -> capacitance W_S = (SA / lam) SA^T + nu^2 I (m x m), same.
+// apply: dense    out = L^-T (L^-1 z)              (two triangular row GEMVs)
+//        woodbury out = (y - SA^T L^-T L^-1 SA y / lam) / nu^2,  y = z / lam
+#include "blas2.cuh"
+#include "chol.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "precond.cuh"
+
+namespace adask {
+
+__global__ void k_recip(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = 1.0 / v[i];
+}
+
+int precond_apply_impl(adask_ctx* ctx, const adask_precond* P, const double* Z, int64_t c,
+                       int64_t ldz, double* out, int64_t ldo, cudaStream_t st) {
+  if (!P) return fail(ADASK_E_ARG, "null preconditioner");
+  if (c < 1 || ldz < P->d || ldo < P->d) return fail(ADASK_E_DIM, "precond_apply: bad shape");
+  for (int64_t j = 0; j < c; ++j) {
+    const double* z = Z + j * ldz;
+    double* o = out + j * ldo;
+    if (P->path == 0) {
+      void* wsp = nullptr;
+      ADASK_TRY(ctx->ws[WS_APPLY].get((size_t)P->k * sizeof(double), st, &wsp));
+      double* t = (double*)wsp;
+      ADASK_TRY(gemv_rows(ctx, P->dtype, P->Linv, P->k, P->k, P->k, z, 1.0, t, 1, st));
+      ADASK_TRY(gemv_rows(ctx, P->dtype, P->LinvT, P->k, P->k, P->k, t, 1.0, o, 2, st));
+    } else {
+      ADASK_TRY(woodbury_apply(ctx, P->dtype, P->SA, P->m, P->d, P->ldsa, P->Linv, P->LinvT, P->k,
+                               P->lam, P->nu2, z, o, st));
+    }
+  }
+  return ADASK_OK;
+}
+
+static void free_precond(adask_precond* P) {
+  if (!P) return;
+  if (P->lam) cudaFree(P->lam);
+  if (P->L) cudaFree(P->L);
+  if (P->Linv) cudaFree(P->Linv);
+  if (P->LinvT) cudaFree(P->LinvT);
+  delete P;
+}
+
+}  // namespace adask
+
+using namespace adask;
+
+extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t d,
+                                   int64_t ldsa, double nu, const double* lam, adask_precond** out,
+                                   int64_t* info_host, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (!out || !lam || (m > 0 && !SA)) return fail(ADASK_E_ARG, "precond_build: null argument");
+  if (m < 1 || d < 1 || ldsa < d) return fail(ADASK_E_DIM, "precond_build: bad shape m=%lld d=%lld",
+                                              (long long)m, (long long)d);
+  if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
+  cudaStream_t st = S(stream);
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  adask_precond* P = new adask_precond();
+  P->device = ctx->device;
+  P->dtype = dtype;
+  P->path = m >= d ? 0 : 1;
+  P->m = m;
+  P->d = d;
+  P->k = m >= d ? d : m;
+  P->SA = SA;
+  P->ldsa = ldsa;
+  P->nu = nu;
+  P->nu2 = nu * nu;
+  const int64_t k = P->k;
+  cudaError_t e = cudaMalloc(&P->lam, (size_t)d * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&P->L, (size_t)k * k * esz);
+  if (e == cudaSuccess) e = cudaMalloc(&P->Linv, (size_t)k * k * esz);
+  if (e == cudaSuccess) e = cudaMalloc(&P->LinvT, (size_t)k * k * esz);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    free_precond(P);
+    return fail(ADASK_E_NOMEM, "precond_build: cudaMalloc: %s", cudaGetErrorString(e));
+  }
+  int s = ADASK_OK;
+  do {
+    e = cudaMemcpyAsync(P->lam, lam, (size_t)d * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+      s = fail(ADASK_E_CUDA, "copy lam: %s", cudaGetErrorString(e));
+      break;
+    }
+    void* wsp = nullptr;
+    const size_t gram_bytes = align_up((size_t)k * k * esz, 256);
+    s = ctx->ws[WS_GRAM].get(gram_bytes + (size_t)d * sizeof(double), st, &wsp);
+    if (s) break;
+    void* M = wsp;
+    double* kinv = (double*)((char*)wsp + gram_bytes);
+    if (P->path == 0) {
+      // H_S = SA^T SA + nu^2 diag(lam)   (preconditioner.py:70)
+      s = gemm_impl(ctx, dtype, d, d, m, 1.0, SA, ldsa, true, SA, ldsa, false, nullptr, 0.0, M, d,
+                    P->nu2, P->lam, true, st);
+    } else {
+      // W_S = (SA * (1/lam)) SA^T + nu^2 I   (preconditioner.py:72-73)
+      k_recip<<<(unsigned)cdiv(d, 256), 256, 0, st>>>(P->lam, d, kinv);
+      cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) {
+        s = fail(ADASK_E_CUDA, "k_recip: %s", cudaGetErrorString(le));
+        break;
+      }
+      ctx->launches++;
+      s = gemm_impl(ctx, dtype, m, m, d, 1.0, SA, ldsa, false, SA, ldsa, true, kinv, 0.0, M, m,
+                    P->nu2, nullptr, true, st);
+    }
+    if (s) break;
+    s = cholesky_inplace(ctx, dtype, M, k, k, P->L, k, P->Linv, k, info_host, st);
+    if (s) break;
+    s = transpose_impl(ctx, dtype, P->Linv, k, k, P->LinvT, k, st);
+  } while (0);
+  if (s != ADASK_OK) {
+    cudaStreamSynchronize(st);
+    free_precond(P);
+    return s;
+  }
+  *out = P;
+  return ADASK_OK;
+}
+
+extern "C" int adask_precond_destroy(adask_precond* P) {
+  if (!P) return ADASK_OK;
+  int cur = -1;
+  const int dev = P->device;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  free_precond(P);  // cudaFree synchronises the device
+  if (cur >= 0 && cur != dev) cudaSetDevice(cur);
+  return ADASK_OK;
+}
+
+extern "C" int adask_precond_path(const adask_precond* P) { return P ? P->path : -1; }
+
+extern "C" int adask_precond_factor(const adask_precond* P, const void** L, int64_t* k, int* dtype) {
+  if (!P) return fail(ADASK_E_ARG, "null preconditioner");
+  if (L) *L = P->L;
+  if (k) *k = P->k;
+  if (dtype) *dtype = P->dtype;
+  return ADASK_OK;
+}
+
+extern "C" int adask_precond_apply(adask_ctx* ctx, const adask_precond* P, const double* Z, int64_t c,
+                                   int64_t ldz, double* out, int64_t ldo, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  return precond_apply_impl(ctx, P, Z, c, ldz, out, ldo, S(stream));
+}
+
+namespace adask {
+template <typename T>
+__global__ void k_mirror_lower(T* M, int64_t k, int64_t ld) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * k) return;
+  int64_t i = e / k, j = e % k;
+  if (j > i) M[i * ld + j] = M[j * ld + i];
+}
+}  // namespace adask
+
+extern "C" int adask_gram(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                          double nu2, const double* lam, void* out, int64_t ldo, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (n < 0 || d < 1 || lda < d || ldo < d) return fail(ADASK_E_DIM, "gram: bad shape");
+  cudaStream_t st = S(stream);
+  ADASK_TRY(gemm_impl(ctx, dtype, d, d, n, 1.0, A, lda, true, A, lda, false, nullptr, 0.0, out, ldo,
+                      lam ? nu2 : 0.0, lam, true, st));
+  if (dtype == ADASK_F64)
+    k_mirror_lower<double><<<(unsigned)cdiv(d * d, 256), 256, 0, st>>>((double*)out, d, ldo);
+  else
+    k_mirror_lower<float><<<(unsigned)cdiv(d * d, 256), 256, 0, st>>>((float*)out, d, ldo);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
+extern "C" int adask_precond_copy_factor(adask_ctx* ctx, const adask_precond* P, int which, void* dst,
+                                         int64_t ldd, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (!P || !dst || ldd < P->k) return fail(ADASK_E_ARG, "copy_factor: bad arguments");
+  const size_t esz = P->dtype == ADASK_F64 ? 8 : 4;
+  const void* src = which == 0 ? P->L : which == 1 ? P->Linv : P->LinvT;
+  ADASK_CUDA(cudaMemcpy2DAsync(dst, (size_t)ldd * esz, src, (size_t)P->k * esz, (size_t)P->k * esz,
+                               (size_t)P->k, cudaMemcpyDeviceToDevice, S(stream)));
+  return ADASK_OK;
+}

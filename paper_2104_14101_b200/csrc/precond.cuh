@@ -1,0 +1,21 @@
+#pragma once
+#include "common.cuh"
+
+struct adask_precond {
+  int device;
+  int dtype;
+  int path;  // 0 cholesky-d, 1 woodbury-m
+  int64_t m, d, k;
+  const void* SA;
+  int64_t ldsa;
+  double nu, nu2;
+  double* lam;   // device copy, d
+  void* L;       // k x k lower
+  void* Linv;    // k x k lower
+  void* LinvT;   // k x k upper (transpose of Linv)
+};
+
+namespace adask {
+int precond_apply_impl(adask_ctx* ctx, const adask_precond* P, const double* Z, int64_t c,
+                       int64_t ldz, double* out, int64_t ldo, cudaStream_t st);
+}  // namespace adask

@@ -1,0 +1,423 @@
+// SRHT  S*A = sqrt(n_pad/m) * R H E A             reference: embeddings.py:81-102
+// and the natural-order Walsh-Hadamard transform         reference: linalg.py:62-88
+//
+// Reference: signs = integers(0, 2, n); Y = fwht(pad(A * signs)) / sqrt(n_pad)
+// (butterfly stages h = 1, 2, 4, ...: y[j] + y[j+h], y[j] - y[j+h]); idx =
+// choice(n_pad, m, replace=False); SA = Y[idx] * sqrt(n_pad / m).
+//
+// The butterfly DAG fixes every output's floating-point evaluation tree, so
+// any schedule that applies the stages in the same bit order reproduces the
+// reference bitwise.  We split the L = log2(n_pad) bits into
+//   pass 1: bits [0, b1) inside blocks of B = 2^b1 rows (one CTA per block and
+//           column panel; 5-bit radix rounds in registers, SMEM between
+//           rounds), fused with the sign flip and zero padding, writing only
+//           the rows whose low b1 bits occur in idx ("slots") to Z;
+//   pass 2: bits [b1, L) across the G = n_pad/B blocks for each needed slot,
+//           writing only the idx rows, scaled by (v / sqrt(n_pad)) * sqrt(n_pad/m)
+//           exactly as the reference's two steps.
+// Algorithmic bytes: (n + m) * d * sizeof(T); the pruned intermediate adds
+// 2 * nslots * G * d * sizeof(T) (nslots <= min(m, B)).
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "rng.cuh"
+#include "srht.cuh"
+
+namespace adask {
+
+enum { FW_P1 = 0, FW_P2 = 1 };
+
+struct FwhtArgs {
+  // pass 1 input: rows of A (global row = blk*B + r), signs (0/1 or null)
+  const void* src;
+  int64_t src_ld;
+  int64_t n_valid;  // rows >= n_valid read as zero (padding)
+  const int32_t* sgn;
+  // pass 1 output: Z[(slot*G + blk) * d + c]; lo_to_slot null = identity
+  const int32_t* lo_to_slot;
+  void* Z;
+  int64_t G;
+  int64_t d;
+  // pass 2 output
+  const int32_t* slot_start;
+  const int32_t* ent_hi;
+  const int32_t* ent_k;
+  void* out;
+  int64_t ldo;
+  double c1, c2;  // out = (v / c1) * c2 ; c2 == 0 -> out = v / c1 ; c1 == 0 -> out = v
+  int accumulate;
+};
+
+template <typename T>
+struct FwTile {
+  static constexpr int minC = 32 / (int)sizeof(T);  // >= one 32-byte sector per row
+};
+
+template <int LOG>
+struct FwShape {
+  static constexpr int B = 1 << LOG;
+  static constexpr int NB1 = LOG < 5 ? LOG : 5;  // bits of round 0
+  static constexpr int E1 = 1 << NB1;
+  static constexpr int ROUNDS = LOG == 0 ? 1 : (LOG + 4) / 5;
+};
+
+template <typename T, int LOG>
+__host__ __device__ constexpr int fw_cols() {
+  constexpr int c = 256 * FwShape<LOG>::E1 / FwShape<LOG>::B;
+  return c > FwTile<T>::minC ? c : FwTile<T>::minC;
+}
+
+// SMEM bytes of the transform tile (unused when one register round suffices).
+template <typename T, int LOG>
+__host__ __device__ constexpr size_t fw_tile_bytes() {
+  return FwShape<LOG>::ROUNDS > 1 ? sizeof(T) * (size_t)FwShape<LOG>::B * fw_cols<T, LOG>() : 0;
+}
+
+__device__ __forceinline__ int fw_row(int q, int e, int lo, int hi) {
+  return (q & ((1 << lo) - 1)) | (e << lo) | ((q >> lo) << hi);
+}
+
+template <typename T, int NB>
+__device__ __forceinline__ void butterflies(T* v) {
+#pragma unroll
+  for (int s = 0; s < NB; ++s) {
+    const int h = 1 << s;
+#pragma unroll
+    for (int e = 0; e < (1 << NB); ++e) {
+      if (!(e & h)) {
+        T a = v[e], b = v[e + h];
+        v[e] = a + b;
+        v[e + h] = a - b;
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T fw_scale(T v, double c1, double c2) {
+  if (c1 == 0.0) return v;
+  if constexpr (sizeof(T) == 8) {
+    double r = __ddiv_rn((double)v, c1);
+    if (c2 != 0.0) r = __dmul_rn(r, c2);
+    return (T)r;
+  } else {
+    float r = __fdiv_rn((float)v, (float)c1);
+    if (c2 != 0.0) r = __fmul_rn(r, (float)c2);
+    return (T)r;
+  }
+}
+
+// Round over bits [lo, lo+NB) of the tile (SMEM in/out), all units.
+template <typename T, int LOG, int NB>
+__device__ __forceinline__ void fw_round_smem(T* tile, int lo) {
+  constexpr int C = fw_cols<T, LOG>();
+  constexpr int CP = C;  // row pitch
+  constexpr int E = 1 << NB;
+  constexpr int UNITS = FwShape<LOG>::B * C / E;
+  const int hi = lo + NB;
+  for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
+    const int c = u % C, q = u / C;
+    T v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = tile[fw_row(q, e, lo, hi) * CP + c];
+    butterflies<T, NB>(v);
+#pragma unroll
+    for (int e = 0; e < E; ++e) tile[fw_row(q, e, lo, hi) * CP + c] = v[e];
+  }
+}
+
+template <typename T, int LOG, int MODE>
+__global__ void __launch_bounds__(256) k_fwht_tile(FwhtArgs a) {
+  using Sh = FwShape<LOG>;
+  constexpr int B = Sh::B;
+  constexpr int C = fw_cols<T, LOG>();
+  constexpr int CP = C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);
+  int* hi_to_k = reinterpret_cast<int*>(smem_raw + fw_tile_bytes<T, LOG>());
+
+  const int64_t blk = blockIdx.x;  // pass 1: row block; pass 2: slot
+  const int64_t c0 = (int64_t)blockIdx.y * C;
+  const int64_t d = a.d;
+
+  if constexpr (MODE == FW_P2) {
+    for (int i = threadIdx.x; i < B; i += blockDim.x) hi_to_k[i] = -1;
+    __syncthreads();
+    const int p0 = a.slot_start[blk], p1 = a.slot_start[blk + 1];
+    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) hi_to_k[a.ent_hi[p]] = a.ent_k[p];
+    __syncthreads();
+  }
+
+  // ---- round 0: global -> registers -> butterflies (bits [0, NB1)) -> SMEM
+  {
+    constexpr int NB = Sh::NB1;
+    constexpr int E = 1 << NB;
+    constexpr int UNITS = B * C / E;
+    for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
+      const int c = u % C, q = u / C;
+      const int64_t col = c0 + c;
+      T v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int r = fw_row(q, e, 0, NB);
+        T x = (T)0;
+        if (col < d) {
+          if constexpr (MODE == FW_P1) {
+            const int64_t grow = blk * B + r;
+            if (grow < a.n_valid) {
+              x = reinterpret_cast<const T*>(a.src)[grow * a.src_ld + col];
+              if (a.sgn) x = a.sgn[grow] ? x : -x;  // diag(signs) A, exact
+            }
+          } else {
+            x = reinterpret_cast<const T*>(a.Z)[(blk * a.G + r) * d + col];
+          }
+        }
+        v[e] = x;
+      }
+      butterflies<T, NB>(v);
+      if constexpr (Sh::ROUNDS == 1) {
+        // output directly
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int r = fw_row(q, e, 0, NB);
+          if (col >= d) continue;
+          if constexpr (MODE == FW_P1) {
+            const int slot = a.lo_to_slot ? a.lo_to_slot[r] : r;
+            if (slot >= 0) reinterpret_cast<T*>(a.Z)[((int64_t)slot * a.G + blk) * d + col] = v[e];
+          } else {
+            const int k = hi_to_k[r];
+            if (k >= 0) {
+              T* o = reinterpret_cast<T*>(a.out) + (int64_t)k * a.ldo + col;
+              T y = fw_scale<T>(v[e], a.c1, a.c2);
+              *o = a.accumulate ? (T)(*o + y) : y;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) tile[fw_row(q, e, 0, NB) * CP + c] = v[e];
+      }
+    }
+  }
+  if constexpr (Sh::ROUNDS == 1) return;
+  // ---- middle rounds in SMEM
+  if constexpr (Sh::ROUNDS >= 3) {
+    __syncthreads();
+    fw_round_smem<T, LOG, 5>(tile, 5);
+  }
+  __syncthreads();
+  // ---- last round: SMEM -> registers -> butterflies -> output
+  {
+    constexpr int LO = 5 * (Sh::ROUNDS - 1);
+    constexpr int NB = LOG - LO;
+    constexpr int E = 1 << NB;
+    constexpr int UNITS = B * C / E;
+    for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
+      const int c = u % C, q = u / C;
+      const int64_t col = c0 + c;
+      T v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = tile[fw_row(q, e, LO, LOG) * CP + c];
+      butterflies<T, NB>(v);
+      if (col >= d) continue;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int r = fw_row(q, e, LO, LOG);
+        if constexpr (MODE == FW_P1) {
+          const int slot = a.lo_to_slot ? a.lo_to_slot[r] : r;
+          if (slot >= 0) reinterpret_cast<T*>(a.Z)[((int64_t)slot * a.G + blk) * d + col] = v[e];
+        } else {
+          const int k = hi_to_k[r];
+          if (k >= 0) {
+            T* o = reinterpret_cast<T*>(a.out) + (int64_t)k * a.ldo + col;
+            T y = fw_scale<T>(v[e], a.c1, a.c2);
+            *o = a.accumulate ? (T)(*o + y) : y;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int LOG, int MODE>
+static int launch_fw(adask_ctx* ctx, const FwhtArgs& a, int64_t nblk, cudaStream_t st) {
+  constexpr int C = fw_cols<T, LOG>();
+  constexpr int B = 1 << LOG;
+  size_t smem = fw_tile_bytes<T, LOG>() + (MODE == FW_P2 ? sizeof(int) * (size_t)B : 0);
+  auto kern = k_fwht_tile<T, LOG, MODE>;
+  if (smem > 48 * 1024) ADASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)nblk, (unsigned)cdiv(a.d, C));
+  kern<<<grid, 256, smem, st>>>(a);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
+template <typename T, int MODE>
+static int dispatch_fw(adask_ctx* ctx, int log, const FwhtArgs& a, int64_t nblk, cudaStream_t st) {
+  switch (log) {
+#define CASE(L) \
+  case L:       \
+    return launch_fw<T, L, MODE>(ctx, a, nblk, st);
+    CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10)
+    CASE(11) CASE(12)
+#undef CASE
+    default:
+      return fail(ADASK_E_ARG, "fwht: block log %d unsupported", log);
+  }
+}
+
+static int ilog2(int64_t n) {
+  int l = 0;
+  while ((1ll << l) < n) ++l;
+  return l;
+}
+
+// Shared driver: pass 1 over all G row blocks (pruned to the slots), pass 2
+// over the slots, writing the requested rows.  idx = output row selection
+// (m entries, values in [0, n_pad)); idx == null means all n_pad rows in order.
+static int fwht_select(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                       const int32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m,
+                       void* out, int64_t ldo, double c1, double c2, int accumulate,
+                       cudaStream_t st) {
+  const int L = ilog2(n_pad);
+  const int b1 = std::max(std::min(L, 10), L - 12);
+  const int64_t B = 1ll << b1, G = n_pad >> b1;
+  const int L2 = L - b1;
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+
+  // ---- host plan (integer bookkeeping, O(m + B))
+  std::vector<int32_t> lo_to_slot((size_t)B, -1);
+  std::vector<int32_t> plan;  // [lo_to_slot B | slot_start nslots+1 | ent_hi m | ent_k m]
+  int64_t nslots = 0;
+  std::vector<int32_t> slot_start, ent_hi, ent_k;
+  if (idx) {
+    for (int64_t k = 0; k < m; ++k) {
+      int64_t lo = idx[k] & (B - 1);
+      if (lo_to_slot[(size_t)lo] < 0) lo_to_slot[(size_t)lo] = 0;
+    }
+    for (int64_t lo = 0; lo < B; ++lo)
+      if (lo_to_slot[(size_t)lo] == 0) lo_to_slot[(size_t)lo] = (int32_t)nslots++;
+    slot_start.assign((size_t)nslots + 1, 0);
+    for (int64_t k = 0; k < m; ++k) slot_start[(size_t)lo_to_slot[(size_t)(idx[k] & (B - 1))] + 1]++;
+    for (int64_t s = 0; s < nslots; ++s) slot_start[(size_t)s + 1] += slot_start[(size_t)s];
+    ent_hi.assign((size_t)m, 0);
+    ent_k.assign((size_t)m, 0);
+    std::vector<int32_t> fillp(slot_start.begin(), slot_start.end() - 1);
+    for (int64_t k = 0; k < m; ++k) {
+      int32_t s = lo_to_slot[(size_t)(idx[k] & (B - 1))];
+      int32_t p = fillp[(size_t)s]++;
+      ent_hi[(size_t)p] = (int32_t)(idx[k] >> b1);
+      ent_k[(size_t)p] = (int32_t)k;
+    }
+  } else {
+    nslots = B;
+    for (int64_t lo = 0; lo < B; ++lo) lo_to_slot[(size_t)lo] = (int32_t)lo;
+    slot_start.resize((size_t)B + 1);
+    for (int64_t s = 0; s <= B; ++s) slot_start[(size_t)s] = (int32_t)(s * G);
+    ent_hi.resize((size_t)n_pad);
+    ent_k.resize((size_t)n_pad);
+    for (int64_t s = 0; s < B; ++s)
+      for (int64_t h = 0; h < G; ++h) {
+        ent_hi[(size_t)(s * G + h)] = (int32_t)h;
+        ent_k[(size_t)(s * G + h)] = (int32_t)((h << b1) | s);
+      }
+    m = n_pad;
+  }
+  plan.reserve((size_t)(B + nslots + 1 + 2 * m));
+  plan.insert(plan.end(), lo_to_slot.begin(), lo_to_slot.end());
+  plan.insert(plan.end(), slot_start.begin(), slot_start.end());
+  plan.insert(plan.end(), ent_hi.begin(), ent_hi.end());
+  plan.insert(plan.end(), ent_k.begin(), ent_k.end());
+  void* pw = nullptr;
+  ADASK_TRY(ctx->ws[WS_PLAN].get(plan.size() * 4, st, &pw));
+  ADASK_CUDA(cudaMemcpyAsync(pw, plan.data(), plan.size() * 4, cudaMemcpyHostToDevice, st));
+  const int32_t* d_lo = (const int32_t*)pw;
+  const int32_t* d_ss = d_lo + B;
+  const int32_t* d_hi = d_ss + nslots + 1;
+  const int32_t* d_k = d_hi + m;
+
+  void* zw = nullptr;
+  ADASK_TRY(ctx->ws[WS_SRHT].get((size_t)nslots * G * d * esz, st, &zw));
+
+  FwhtArgs a{};
+  a.src = A;
+  a.src_ld = lda;
+  a.n_valid = n;
+  a.sgn = sgn;
+  a.lo_to_slot = d_lo;
+  a.Z = zw;
+  a.G = G;
+  a.d = d;
+  if (dtype == ADASK_F64)
+    ADASK_TRY((dispatch_fw<double, FW_P1>(ctx, b1, a, G, st)));
+  else
+    ADASK_TRY((dispatch_fw<float, FW_P1>(ctx, b1, a, G, st)));
+  a.slot_start = d_ss;
+  a.ent_hi = d_hi;
+  a.ent_k = d_k;
+  a.out = out;
+  a.ldo = ldo;
+  a.c1 = c1;
+  a.c2 = c2;
+  a.accumulate = accumulate;
+  if (dtype == ADASK_F64)
+    ADASK_TRY((dispatch_fw<double, FW_P2>(ctx, L2, a, nslots, st)));
+  else
+    ADASK_TRY((dispatch_fw<float, FW_P2>(ctx, L2, a, nslots, st)));
+  // the host plan vector must outlive the (pageable, staged) copy: it does,
+  // cudaMemcpyAsync from pageable memory returns after staging.
+  return ADASK_OK;
+}
+
+int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                     const adask_pcg64* g, int64_t m, void* SA, int64_t ldsa, int64_t* idx_host,
+                     uint32_t flags, cudaStream_t st) {
+  if (m < 1) return fail(ADASK_E_SKETCH_TOO_LARGE, "sketch size must be a positive integer, got %lld",
+                         (long long)m);
+  if (n < 1 || d < 1 || lda < d || ldsa < d) return fail(ADASK_E_DIM, "sketch_srht: bad shape");
+  if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
+  const int64_t n_pad = 1ll << ilog2(n);
+  if (m > n_pad)
+    return fail(ADASK_E_SKETCH_TOO_LARGE, "m = %lld exceeds padded row count %lld", (long long)m,
+                (long long)n_pad);
+  if (ilog2(n_pad) > 24) return fail(ADASK_E_ARG, "sketch_srht: n_pad > 2^24 unsupported");
+  // signs: draws [0, n) of integers(0, 2)
+  void* sw = nullptr;
+  ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)n * 4, st, &sw));
+  int32_t* sgn = (int32_t*)sw;
+  ADASK_TRY(pcg_integers_impl(ctx, g, 0, 0, n, n, 2u, sgn, nullptr, st));
+  // idx = choice(n_pad, m, replace=False) after the n sign draws (host)
+  adask_pcg64 h = *g;
+  adask_pcg64_skip_u32(&h, (uint64_t)n);
+  std::vector<int64_t> idx((size_t)m);
+  ADASK_TRY(adask_choice_noreplace(&h, n_pad, m, idx.data()));
+  if (idx_host) std::copy(idx.begin(), idx.end(), idx_host);
+  const double c1 = sqrt((double)n_pad);
+  const double c2 = sqrt((double)n_pad / (double)m);
+  return fwht_select(ctx, dtype, A, n, d, lda, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2,
+                     (flags & ADASK_ACCUMULATE) ? 1 : 0, st);
+}
+
+}  // namespace adask
+
+using namespace adask;
+
+extern "C" int adask_sketch_srht(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d,
+                                 int64_t lda, const adask_pcg64* g, int64_t m, void* SA,
+                                 int64_t ldsa, int64_t* idx_host, uint32_t flags, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (!g) return fail(ADASK_E_ARG, "null generator");
+  return sketch_srht_impl(ctx, dtype, A, n, d, lda, g, m, SA, ldsa, idx_host, flags, S(stream));
+}
+
+extern "C" int adask_fwht(adask_ctx* ctx, int dtype, void* X, int64_t n, int64_t d, int64_t ldx,
+                          int normalized, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (n < 1 || (n & (n - 1))) return fail(ADASK_E_NOT_POW2, "length %lld is not a power of two", (long long)n);
+  if (d < 1 || ldx < d) return fail(ADASK_E_DIM, "fwht: bad shape");
+  if (ilog2(n) > 24) return fail(ADASK_E_ARG, "fwht: n > 2^24 unsupported");
+  // pass 1 reads X, the intermediate lives in WS_SRHT, pass 2 overwrites X.
+  const double c1 = normalized ? sqrt((double)n) : 0.0;
+  return fwht_select(ctx, dtype, X, n, d, ldx, nullptr, n, nullptr, n, X, ldx, c1, 0.0, 0, S(stream));
+}

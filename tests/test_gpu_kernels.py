@@ -1,0 +1,155 @@
+"""GPU parity of every libadask kernel against the CPU oracle (oracle/)
+on seeded inputs.  Integer/index work and the SRHT/SJLT sketches are
+bit-exact; floating-point reductions are checked at the stated tolerances."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import adasketch_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ak():
+    import paper_2104_14101_b200 as ak
+
+    return ak
+
+
+def _dev_integers(seed, first, count, m):
+    from paper_2104_14101_b200 import _lib
+    from paper_2104_14101_b200 import device as dv
+
+    g = _lib.pcg64_from_seed(seed)
+    out = torch.empty(count, dtype=torch.int32, device="cuda")
+    nxt = C.c_uint64()
+    _lib.check(_lib.lib().adask_pcg64_integers(dv.ctx().handle, C.byref(g), first, count, m,
+                                               out.data_ptr(), C.byref(nxt), dv.stream()))
+    return out.cpu().numpy().astype(np.int64), int(nxt.value)
+
+
+@pytest.mark.parametrize("m", [2, 64, 65536, 1, 3, 1000, 2**31 + 1])
+def test_pcg64_integers_bit_exact(ak, m):
+    n = 20000
+    ref = np.random.default_rng(77).integers(0, m, size=n)
+    got, nxt = _dev_integers(77, 0, n, m)
+    assert np.array_equal(got, ref)
+
+
+def test_pcg64_integers_offset_and_next(ak):
+    # buckets then signs from one stream (embeddings.py:118, 124) for odd n
+    n, m = 1001, 3
+    rng = np.random.default_rng(5)
+    rows = rng.integers(0, m, size=n)
+    signs = rng.integers(0, 2, size=n)
+    got_rows, nxt = _dev_integers(5, 0, n, m)
+    got_signs, _ = _dev_integers(5, nxt, n, 2)
+    assert np.array_equal(got_rows, rows)
+    assert np.array_equal(got_signs, signs)
+
+
+def test_philox_gaussian_matches_oracle(ak):
+    S = ak.gaussian_matrix(7, 301, seed=2**40 + 17, col0=5).cpu().numpy()
+    ref = O.philox_gaussian(7, 301, 2**40 + 17, col0=5)
+    np.testing.assert_allclose(S, ref, rtol=1e-14, atol=1e-15)
+    assert abs(S.std() * np.sqrt(7) - 1.0) < 0.1
+
+
+@pytest.mark.parametrize("n,d", [(100, 5), (4096, 256), (1000, 37), (513, 1024), (300, 2048),
+                                 (77, 4096), (50, 5000), (1, 3)])
+def test_hess_mult_fp64(ak, n, d):
+    rng = np.random.default_rng(n * 7 + d)
+    A = rng.standard_normal((n, d))
+    lam = 1.0 + rng.uniform(0, 3, d)
+    B = rng.standard_normal((d, 2))
+    X = rng.standard_normal((d, 2))
+    p = ak.RegularizedProblem(A, B, 0.3, lam)
+    po = O.Problem.make(A, B, 0.3, lam)
+    for got, ref in ((p.hess_mult(X), po.hess_mult(X)), (p.gradient(X), po.gradient(X)),
+                     (p.hess_mult(X[:, 0]), po.hess_mult(X[:, 0]))):
+        assert got.shape == ref.shape
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("n,d", [(1000, 256), (4099, 1024), (300, 4096), (64, 3)])
+def test_hess_mult_fp32(ak, n, d):
+    rng = np.random.default_rng(d)
+    A = rng.standard_normal((n, d)).astype(np.float32)
+    X = rng.standard_normal(d)
+    p = ak.RegularizedProblem(A, np.zeros(d), 0.5, dtype="float32")
+    ref = O.Problem.make(A.astype(np.float64), np.zeros(d), 0.5).hess_mult(X)
+    got = p.hess_mult(X)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)  # fp64 accumulation of fp32 data
+
+
+@pytest.mark.parametrize("n,d,m,seed", [(64, 5, 16, 9), (1000, 37, 64, 3), (5000, 129, 1000, 4),
+                                        (1 << 14, 256, 4096, 5), (20, 8, 1, 2), (333, 16, 333, 8)])
+def test_sjlt_bitwise(ak, n, d, m, seed):
+    A = np.random.default_rng(seed).standard_normal((n, d))
+    got = ak.sketch_sjlt(A, m, seed).SA
+    ref = O.sketch_sjlt(A, m, seed)
+    assert np.array_equal(got, ref)
+
+
+def test_sjlt_s_gt_1(ak):
+    A = np.random.default_rng(1).standard_normal((200, 6))
+    got = ak.sketch_sjlt(A, 16, 25, s=3).SA
+    ref = O.sketch_sjlt(A, 16, 25, s=3)
+    np.testing.assert_allclose(got, ref, rtol=1e-15, atol=1e-15)
+    S = ak.sketch_sjlt(np.eye(30), 16, seed=25, s=3).SA
+    assert np.array_equal((S != 0).sum(axis=0), np.full(30, 3))
+
+
+@pytest.mark.parametrize("n,d,m,seed", [(64, 3, 64, 4), (300, 4, 128, 1), (1000, 7, 500, 2),
+                                        (4096, 33, 256, 3), (5000, 17, 3000, 6), (1, 2, 1, 0),
+                                        (1 << 16, 8, 32, 11), (70000, 5, 4096, 12)])
+def test_srht_bitwise(ak, n, d, m, seed):
+    A = np.random.default_rng(seed).standard_normal((n, d))
+    got = ak.sketch_srht(A, m, seed).SA
+    ref = O.sketch_srht(A, m, seed)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("n,d", [(1, 1), (8, 3), (1024, 5), (4096, 2), (1 << 15, 3)])
+def test_fwht_bitwise(ak, n, d):
+    x = np.random.default_rng(n).standard_normal((n, d))
+    assert np.array_equal(ak.fwht(x), O.fwht(x))
+    assert np.array_equal(ak.fwht(x, normalized=False), O.fwht(x, normalized=False))
+
+
+def test_gaussian_sketch_matches_injected_oracle(ak):
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((4096, 256))
+    for m in (16, 256, 300):
+        got = ak.sketch_gaussian(A, m, 1234).SA
+        ref = O.sketch_gaussian(A, m, 1234)
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("m,d", [(40, 10), (10, 10), (6, 10), (300, 200), (100, 300), (700, 129)])
+def test_precond_solve_both_paths(ak, m, d):
+    rng = np.random.default_rng(m + d)
+    SA = rng.standard_normal((m, d))
+    lam = 1.0 + rng.uniform(0, 2, d)
+    nu = 0.7
+    P = ak.build(SA, nu, lam)
+    Po = O.build(SA, nu, lam)
+    assert P.path == Po.path
+    Z = rng.standard_normal((d, 3))
+    got, ref = P.solve(Z), Po.solve(Z)
+    assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+    np.testing.assert_allclose(P.L, Po.L, rtol=1e-9, atol=1e-12)
+
+
+def test_cholesky_not_spd(ak):
+    from paper_2104_14101_b200.errors import NotPositiveDefinite
+
+    M = np.eye(100)
+    M[57, 57] = -1.0
+    with pytest.raises(NotPositiveDefinite):
+        ak.cholesky(M)
+    L = ak.cholesky(np.array([[4.0, 2.0], [2.0, 3.0]]))
+    np.testing.assert_allclose(L, [[2.0, 0.0], [1.0, np.sqrt(2.0)]])
