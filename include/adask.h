@@ -116,6 +116,15 @@ int adask_ctx_create(int device, adask_ctx** out);
 int adask_ctx_destroy(adask_ctx* ctx);
 /* Kernel launches issued through this ctx since creation (instrumentation). */
 int64_t adask_ctx_launches(const adask_ctx* ctx);
+/* Live timing of work units with CUDA events on the launching stream.
+ * kind: 0 hess_mult, 1 SRHT sketch, 2 SJLT sketch, 3 Gaussian sketch,
+ * 4 preconditioner build, 5 preconditioner apply.  Query synchronises and
+ * returns the number of units, their summed device time and algorithmic
+ * bytes / flops.                                          */
+int adask_prof_enable(adask_ctx* ctx, int on);
+int adask_prof_reset(adask_ctx* ctx);
+int adask_prof_query(adask_ctx* ctx, int kind, int64_t* count, double* total_ms,
+                     double* total_bytes, double* total_flops);
 
 /* ======================================================================== */
 /* Randomness on the device                                                 */

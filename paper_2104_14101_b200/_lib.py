@@ -80,6 +80,9 @@ _PROTOS = {
     "adask_ctx_create": (C.c_int, [C.c_int, P(vp)]),
     "adask_ctx_destroy": (C.c_int, [vp]),
     "adask_ctx_launches": (i64, [vp]),
+    "adask_prof_enable": (C.c_int, [vp, C.c_int]),
+    "adask_prof_reset": (C.c_int, [vp]),
+    "adask_prof_query": (C.c_int, [vp, C.c_int, P(i64), P(dbl), P(dbl), P(dbl)]),
     "adask_pcg64_integers": (C.c_int, [vp, P(PCG64State), u64, i64, u32, vp, P(u64), vp]),
     "adask_philox_gaussian": (C.c_int, [vp, C.c_int, i64, i64, i64, u64, vp, i64, vp]),
     "adask_philox_gaussian_host": (C.c_int, [i64, i64, i64, u64, vp, i64]),
@@ -175,6 +178,22 @@ class Context:
 
     def launches(self) -> int:
         return int(lib().adask_ctx_launches(self.handle))
+
+    PROF_KINDS = ("hess_mult", "srht", "sjlt", "gaussian", "build", "apply")
+
+    def prof_enable(self, on: bool = True) -> None:
+        check(lib().adask_prof_enable(self.handle, 1 if on else 0))
+
+    def prof_reset(self) -> None:
+        check(lib().adask_prof_reset(self.handle))
+
+    def prof_query(self) -> dict:
+        out = {}
+        for k, name in enumerate(self.PROF_KINDS):
+            cnt, ms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            check(lib().adask_prof_query(self.handle, k, C.byref(cnt), C.byref(ms), C.byref(by), C.byref(fl)))
+            out[name] = {"count": cnt.value, "ms": ms.value, "bytes": by.value, "flops": fl.value}
+        return out
 
 
 def int_words(v: int) -> list[int]:

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/adask.h"
 
@@ -92,7 +93,25 @@ enum WsSlot {
   WS_COUNT
 };
 
+// Live per-unit timing (CUDA events on the launching stream), enabled by
+// adask_prof_enable; used by bench.py for the roofline of the dominant unit.
+enum ProfKind {
+  PK_HESS = 0,   // fused A^T A pass (hess_mult)
+  PK_SRHT,       // whole SRHT sketch
+  PK_SJLT,       // whole SJLT sketch
+  PK_GAUSS,      // whole Gaussian sketch
+  PK_BUILD,      // preconditioner build (Gram + Cholesky + inverse)
+  PK_APPLY,      // preconditioner apply
+  PK_COUNT
+};
+
 }  // namespace adask
+
+struct adask_prof_rec {
+  cudaEvent_t a, b;
+  double bytes;
+  double flops;
+};
 
 struct adask_ctx {
   int device = 0;
@@ -100,7 +119,45 @@ struct adask_ctx {
   adask::Workspace ws[adask::WS_COUNT];
   double* pinned = nullptr;  // pinned host scalars for synchronous readbacks
   int* pinned_flags = nullptr;
+  int prof = 0;
+  std::vector<adask_prof_rec> prof_recs[adask::PK_COUNT];
+  std::vector<cudaEvent_t> event_pool;
 };
+
+namespace adask {
+// RAII timing scope for one unit; no-op unless profiling is enabled.
+struct ProfScope {
+  adask_ctx* ctx;
+  int kind;
+  cudaStream_t st;
+  adask_prof_rec rec{};
+  bool on;
+  ProfScope(adask_ctx* c, int k, cudaStream_t s, double bytes, double flops = 0.0)
+      : ctx(c), kind(k), st(s), on(c && c->prof) {
+    if (!on) return;
+    rec.a = take();
+    rec.b = take();
+    rec.bytes = bytes;
+    rec.flops = flops;
+    cudaEventRecord(rec.a, st);
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(rec.b, st);
+    ctx->prof_recs[kind].push_back(rec);
+  }
+  cudaEvent_t take() {
+    cudaEvent_t e;
+    if (!ctx->event_pool.empty()) {
+      e = ctx->event_pool.back();
+      ctx->event_pool.pop_back();
+    } else {
+      cudaEventCreate(&e);
+    }
+    return e;
+  }
+};
+}  // namespace adask
 
 namespace adask {
 

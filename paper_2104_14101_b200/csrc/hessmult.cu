@@ -295,6 +295,8 @@ int hess_mult_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t 
                 (long long)d, (long long)c);
   const bool partial = (flags & ADASK_PARTIAL) != 0;
   if (!partial && !lam) return fail(ADASK_E_ARG, "hess_mult: lam required");
+  ProfScope prof(ctx, PK_HESS, st, (double)n * d * (dtype == ADASK_F64 ? 8 : 4) * c,
+                 4.0 * (double)n * d * c);
   for (int64_t j = 0; j < c; ++j) {
     const double* x = X + j * ldx;
     double* part = nullptr;

@@ -372,3 +372,43 @@ int adask_ctx_destroy(adask_ctx* ctx) {
 int64_t adask_ctx_launches(const adask_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 }  // extern "C"
+
+extern "C" int adask_prof_enable(adask_ctx* ctx, int on) {
+  if (!ctx) return fail(ADASK_E_ARG, "null context");
+  ctx->prof = on ? 1 : 0;
+  return ADASK_OK;
+}
+
+extern "C" int adask_prof_reset(adask_ctx* ctx) {
+  if (!ctx) return fail(ADASK_E_ARG, "null context");
+  cudaSetDevice(ctx->device);
+  for (auto& v : ctx->prof_recs) {
+    for (auto& r : v) {
+      ctx->event_pool.push_back(r.a);
+      ctx->event_pool.push_back(r.b);
+    }
+    v.clear();
+  }
+  return ADASK_OK;
+}
+
+// Totals for one unit kind since the last reset (synchronises the device).
+extern "C" int adask_prof_query(adask_ctx* ctx, int kind, int64_t* count, double* total_ms,
+                                double* total_bytes, double* total_flops) {
+  if (!ctx || kind < 0 || kind >= PK_COUNT) return fail(ADASK_E_ARG, "prof_query: bad arguments");
+  ADASK_CUDA(cudaSetDevice(ctx->device));
+  ADASK_CUDA(cudaDeviceSynchronize());
+  double ms = 0, by = 0, fl = 0;
+  for (auto& r : ctx->prof_recs[kind]) {
+    float t = 0;
+    ADASK_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    by += r.bytes;
+    fl += r.flops;
+  }
+  if (count) *count = (int64_t)ctx->prof_recs[kind].size();
+  if (total_ms) *total_ms = ms;
+  if (total_bytes) *total_bytes = by;
+  if (total_flops) *total_flops = fl;
+  return ADASK_OK;
+}

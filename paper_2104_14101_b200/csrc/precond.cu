@@ -23,6 +23,10 @@ int precond_apply_impl(adask_ctx* ctx, const adask_precond* P, const double* Z, 
                        int64_t ldz, double* out, int64_t ldo, cudaStream_t st) {
   if (!P) return fail(ADASK_E_ARG, "null preconditioner");
   if (c < 1 || ldz < P->d || ldo < P->d) return fail(ADASK_E_DIM, "precond_apply: bad shape");
+  const double esz = P->dtype == ADASK_F64 ? 8.0 : 4.0;
+  const double bytes = P->path == 0 ? (double)P->k * P->k * esz
+                                    : (2.0 * P->m * P->d + (double)P->m * P->m) * esz;
+  ProfScope prof(ctx, PK_APPLY, st, bytes * c);
   for (int64_t j = 0; j < c; ++j) {
     const double* z = Z + j * ldz;
     double* o = out + j * ldo;
@@ -30,10 +34,10 @@ int precond_apply_impl(adask_ctx* ctx, const adask_precond* P, const double* Z, 
       void* wsp = nullptr;
       ADASK_TRY(ctx->ws[WS_APPLY].get((size_t)P->k * sizeof(double), st, &wsp));
       double* t = (double*)wsp;
-      ADASK_TRY(gemv_rows(ctx, P->dtype, P->Linv, P->k, P->k, P->k, z, 1.0, t, 1, st));
-      ADASK_TRY(gemv_rows(ctx, P->dtype, P->LinvT, P->k, P->k, P->k, t, 1.0, o, 2, st));
+      ADASK_TRY(gemv_rows(ctx, P->dtype, P->Linv, P->k, P->k, P->kp, z, 1.0, t, 1, st));
+      ADASK_TRY(gemv_rows(ctx, P->dtype, P->LinvT, P->k, P->k, P->kp, t, 1.0, o, 2, st));
     } else {
-      ADASK_TRY(woodbury_apply(ctx, P->dtype, P->SA, P->m, P->d, P->ldsa, P->Linv, P->LinvT, P->k,
+      ADASK_TRY(woodbury_apply(ctx, P->dtype, P->SA, P->m, P->d, P->ldsa, P->Linv, P->LinvT, P->kp,
                                P->lam, P->nu2, z, o, st));
     }
   }
@@ -42,10 +46,8 @@ int precond_apply_impl(adask_ctx* ctx, const adask_precond* P, const double* Z, 
 
 static void free_precond(adask_precond* P) {
   if (!P) return;
-  if (P->lam) cudaFree(P->lam);
-  if (P->L) cudaFree(P->L);
-  if (P->Linv) cudaFree(P->Linv);
-  if (P->LinvT) cudaFree(P->LinvT);
+  // one stream-ordered block: lam | L | Linv | LinvT
+  if (P->lam) cudaFreeAsync(P->lam, P->stream);
   delete P;
 }
 
@@ -75,16 +77,27 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
   P->nu = nu;
   P->nu2 = nu * nu;
   const int64_t k = P->k;
-  cudaError_t e = cudaMalloc(&P->lam, (size_t)d * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&P->L, (size_t)k * k * esz);
-  if (e == cudaSuccess) e = cudaMalloc(&P->Linv, (size_t)k * k * esz);
-  if (e == cudaSuccess) e = cudaMalloc(&P->LinvT, (size_t)k * k * esz);
+  const int64_t kp = cdiv(k, 64) * 64;
+  P->kp = kp;
+  P->stream = st;
+  const size_t lam_bytes = align_up((size_t)d * sizeof(double), 256);
+  const size_t mat = align_up((size_t)kp * kp * esz, 256);
+  char* blk = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&blk, lam_bytes + 3 * mat, st);
+  if (e == cudaSuccess) {
+    P->lam = (double*)blk;
+    P->L = blk + lam_bytes;
+    P->Linv = blk + lam_bytes + mat;
+    P->LinvT = blk + lam_bytes + 2 * mat;
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     free_precond(P);
     return fail(ADASK_E_NOMEM, "precond_build: cudaMalloc: %s", cudaGetErrorString(e));
   }
   int s = ADASK_OK;
+  const double gram_flops = m >= d ? (double)m * d * (d + 1) : (double)m * (m + 1) * d;
+  ProfScope prof(ctx, PK_BUILD, st, (double)m * d * esz, gram_flops + (double)k * k * k / 3.0);
   do {
     e = cudaMemcpyAsync(P->lam, lam, (size_t)d * sizeof(double), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) {
@@ -92,14 +105,14 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
       break;
     }
     void* wsp = nullptr;
-    const size_t gram_bytes = align_up((size_t)k * k * esz, 256);
+    const size_t gram_bytes = align_up((size_t)kp * kp * esz, 256);
     s = ctx->ws[WS_GRAM].get(gram_bytes + (size_t)d * sizeof(double), st, &wsp);
     if (s) break;
     void* M = wsp;
     double* kinv = (double*)((char*)wsp + gram_bytes);
     if (P->path == 0) {
       // H_S = SA^T SA + nu^2 diag(lam)   (preconditioner.py:70)
-      s = gemm_impl(ctx, dtype, d, d, m, 1.0, SA, ldsa, true, SA, ldsa, false, nullptr, 0.0, M, d,
+      s = gemm_impl(ctx, dtype, d, d, m, 1.0, SA, ldsa, true, SA, ldsa, false, nullptr, 0.0, M, kp,
                     P->nu2, P->lam, true, st);
     } else {
       // W_S = (SA * (1/lam)) SA^T + nu^2 I   (preconditioner.py:72-73)
@@ -110,13 +123,13 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
         break;
       }
       ctx->launches++;
-      s = gemm_impl(ctx, dtype, m, m, d, 1.0, SA, ldsa, false, SA, ldsa, true, kinv, 0.0, M, m,
+      s = gemm_impl(ctx, dtype, m, m, d, 1.0, SA, ldsa, false, SA, ldsa, true, kinv, 0.0, M, kp,
                     P->nu2, nullptr, true, st);
     }
     if (s) break;
-    s = cholesky_inplace(ctx, dtype, M, k, k, P->L, k, P->Linv, k, info_host, st);
+    s = pad_identity(ctx, dtype, M, k, kp, st);
     if (s) break;
-    s = transpose_impl(ctx, dtype, P->Linv, k, k, P->LinvT, k, st);
+    s = chol_factor_inverse(ctx, dtype, M, k, kp, P->L, P->Linv, P->LinvT, info_host, st);
   } while (0);
   if (s != ADASK_OK) {
     cudaStreamSynchronize(st);
@@ -133,7 +146,7 @@ extern "C" int adask_precond_destroy(adask_precond* P) {
   const int dev = P->device;
   cudaGetDevice(&cur);
   if (cur != dev) cudaSetDevice(dev);
-  free_precond(P);  // cudaFree synchronises the device
+  free_precond(P);  // stream-ordered free on the build stream
   if (cur >= 0 && cur != dev) cudaSetDevice(cur);
   return ADASK_OK;
 }
@@ -185,7 +198,7 @@ extern "C" int adask_precond_copy_factor(adask_ctx* ctx, const adask_precond* P,
   if (!P || !dst || ldd < P->k) return fail(ADASK_E_ARG, "copy_factor: bad arguments");
   const size_t esz = P->dtype == ADASK_F64 ? 8 : 4;
   const void* src = which == 0 ? P->L : which == 1 ? P->Linv : P->LinvT;
-  ADASK_CUDA(cudaMemcpy2DAsync(dst, (size_t)ldd * esz, src, (size_t)P->k * esz, (size_t)P->k * esz,
+  ADASK_CUDA(cudaMemcpy2DAsync(dst, (size_t)ldd * esz, src, (size_t)P->kp * esz, (size_t)P->k * esz,
                                (size_t)P->k, cudaMemcpyDeviceToDevice, S(stream)));
   return ADASK_OK;
 }

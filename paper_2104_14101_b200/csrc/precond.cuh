@@ -6,6 +6,8 @@ struct adask_precond {
   int dtype;
   int path;  // 0 cholesky-d, 1 woodbury-m
   int64_t m, d, k;
+  int64_t kp;    // k padded to a multiple of 64: leading dimension of L, Linv, LinvT
+  cudaStream_t stream;  // build stream (allocations are stream-ordered on it)
   const void* SA;
   int64_t ldsa;
   double nu, nu2;

@@ -199,6 +199,7 @@ int sketch_sjlt_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n_local, 
   if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
   const int64_t nent = n_local * s;
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  ProfScope prof(ctx, PK_SJLT, st, (double)(n_local + m) * d * esz);
   const int accumulate = (flags & ADASK_ACCUMULATE) ? 1 : 0;
   if (nent == 0) {
     if (!accumulate)

@@ -382,6 +382,7 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
     return fail(ADASK_E_SKETCH_TOO_LARGE, "m = %lld exceeds padded row count %lld", (long long)m,
                 (long long)n_pad);
   if (ilog2(n_pad) > 24) return fail(ADASK_E_ARG, "sketch_srht: n_pad > 2^24 unsupported");
+  ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4));
   // signs: draws [0, n) of integers(0, 2)
   void* sw = nullptr;
   ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)n * 4, st, &sw));

@@ -153,3 +153,26 @@ def test_cholesky_not_spd(ak):
         ak.cholesky(M)
     L = ak.cholesky(np.array([[4.0, 2.0], [2.0, 3.0]]))
     np.testing.assert_allclose(L, [[2.0, 0.0], [1.0, np.sqrt(2.0)]])
+
+
+@pytest.mark.parametrize("m,d", [(3000, 1030), (1500, 2000), (4096, 1024)])
+def test_precond_large(ak, m, d):
+    rng = np.random.default_rng(m)
+    SA = rng.standard_normal((m, d)) / np.sqrt(m)
+    lam = 1.0 + rng.uniform(0, 9, d)
+    P = ak.build(SA, 0.05, lam)
+    Po = O.build(SA, 0.05, lam)
+    z = rng.standard_normal(d)
+    got, ref = P.solve(z), Po.solve(z)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("k", [1, 63, 64, 65, 700, 2500])
+def test_cholesky_sizes(ak, k):
+    rng = np.random.default_rng(k)
+    X = rng.standard_normal((k + 5, k))
+    M = X.T @ X + np.eye(k)
+    L = ak.cholesky(M)
+    Lo = np.linalg.cholesky(M)
+    assert np.linalg.norm(L - Lo) <= 1e-11 * np.linalg.norm(Lo)
+    assert np.allclose(np.triu(L, 1), 0.0)
