@@ -164,6 +164,7 @@ namespace adask {
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+__host__ __device__ inline size_t align_up_dev(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Activate ctx's device for the calling thread.
 int use_device(adask_ctx* ctx);
@@ -174,6 +175,40 @@ __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Reduce R (power of two <= 32) per-lane values across the warp with a
+// recursive-halving exchange: R - 1 + 5 - log2(R) shuffles instead of 5R.
+// Returns the warp total of row `r`, where r = warp_multi_row<R>(lane); every
+// lane with (lane & (32/R - 1)) == 0 holds a distinct row.  Fixed order.
+template <int R>
+__device__ __forceinline__ int warp_multi_row(int lane) {
+  int r = 0, bitpos = 4;
+#pragma unroll
+  for (int h = R; h > 1; h >>= 1) {
+    r = (r << 1) | ((lane >> bitpos) & 1);
+    --bitpos;
+  }
+  return r;
+}
+template <int R>
+__device__ __forceinline__ double warp_multi_sum(double (&v)[R]) {
+  const int lane = threadIdx.x & 31;
+  int off = 16;
+#pragma unroll
+  for (int h = R; h > 1; h >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < h / 2; ++j) {
+      const double send = up ? v[j] : v[j + h / 2];
+      const double keep = up ? v[j + h / 2] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+    off >>= 1;
+  }
+  double t = v[0];
+  for (; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+  return t;
 }
 
 // Deterministic block reduction of one double (fixed tree, any blockDim that is

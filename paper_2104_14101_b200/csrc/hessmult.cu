@@ -12,6 +12,7 @@
 // Algorithmic bytes per call: n * d * sizeof(T).
 #include "common.cuh"
 #include "hessmult.cuh"
+#include "tma.cuh"
 
 namespace adask {
 
@@ -139,6 +140,222 @@ __global__ void __launch_bounds__(256) k_hess_fused(const T* __restrict__ A, int
       int64_t col = c * VEC + v;
       if (col < d) out[col] = acc[ch][v];
     }
+  }
+}
+
+// TMA-fed variant (the B200 path): one CTA per SM, a producer warp streams
+// R-row stages of A into a STAGES-deep SMEM ring with cp.async.bulk
+// (mbarrier completion, L2 evict-first), eight consumer warps read their
+// 16-byte column chunks from SMEM, release the stage, reduce the R row dots
+// across the CTA (one named barrier per stage) and accumulate y_r a_r in
+// registers.  Bytes in flight no longer depend on occupancy or registers.
+template <typename T, int NCH, int R, int STAGES>
+__global__ void __launch_bounds__(288, 1) k_hess_tma(const T* __restrict__ A, int64_t n, int64_t d,
+                                                     int64_t lda, const double* __restrict__ x,
+                                                     double* __restrict__ part) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int NW = 8;  // consumer warps
+  extern __shared__ __align__(128) unsigned char hsm[];
+  const int64_t stage_elems = (int64_t)R * d;
+  T* ring = reinterpret_cast<T*>(hsm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(hsm + align_up_dev(STAGES * stage_elems * sizeof(T), 128));
+  uint64_t* empty = full + STAGES;
+  double* red = reinterpret_cast<double*>(empty + STAGES);  // [2][NW][R]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t row_begin = n * blockIdx.x / gridDim.x, row_end = n * (blockIdx.x + 1) / gridDim.x;
+  const int64_t ntiles = (row_end - row_begin + R - 1) / R;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == NW) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const uint32_t row_bytes = (uint32_t)(d * sizeof(T));
+      for (int64_t t = 0; t < ntiles; ++t) {
+        const int s = (int)(t % STAGES);
+        const uint32_t ph = (uint32_t)((t / STAGES) & 1);
+        if (t >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+        const int64_t r0 = row_begin + t * R;
+        const int rows = (int)min((int64_t)R, row_end - r0);
+        mbar_arrive_expect_tx(&full[s], rows * row_bytes);
+        T* dst = ring + s * stage_elems;
+        if (lda == d) {
+          bulk_g2s_evict_first(dst, A + r0 * lda, rows * row_bytes, &full[s], pol);
+        } else {
+          for (int r = 0; r < rows; ++r)
+            bulk_g2s_evict_first(dst + r * d, A + (r0 + r) * lda, row_bytes, &full[s], pol);
+        }
+      }
+    }
+    return;
+  }
+  const int64_t nchunks = d / V;
+  double xv[NCH][V], acc[NCH][V];
+  bool act[NCH];
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    const int64_t c = (int64_t)ch * (NW * 32) + tid;
+    act[ch] = c < nchunks;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      xv[ch][v] = act[ch] ? x[c * V + v] : 0.0;
+      acc[ch][v] = 0.0;
+    }
+  }
+  int buf = 0;
+  for (int64_t t = 0; t < ntiles; ++t) {
+    const int s = (int)(t % STAGES);
+    const uint32_t ph = (uint32_t)((t / STAGES) & 1);
+    const int rows = (int)min((int64_t)R, row_end - (row_begin + t * R));
+    mbar_wait(&full[s], ph);
+    const T* src = ring + s * stage_elems;
+    T a[R][NCH][V];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int64_t c = (int64_t)ch * (NW * 32) + tid;
+        if (r < rows && act[ch]) {
+          if constexpr (sizeof(T) == 8) {
+            const double2 q = *reinterpret_cast<const double2*>(src + r * d + c * V);
+            a[r][ch][0] = q.x;
+            a[r][ch][1] = q.y;
+          } else {
+            const float4 q = *reinterpret_cast<const float4*>(src + r * d + c * V);
+            a[r][ch][0] = q.x;
+            a[r][ch][1] = q.y;
+            a[r][ch][2] = q.z;
+            a[r][ch][3] = q.w;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) a[r][ch][v] = (T)0;
+        }
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage consumed by this warp
+    double dot[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if constexpr (sizeof(T) == 8) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int v = 0; v < V; ++v) sacc = fma((double)a[r][ch][v], xv[ch][v], sacc);
+        dot[r] = sacc;
+      } else {
+        // fp32 data: short per-thread partial in fp32, reduced in fp64
+        float sacc = 0.0f;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int v = 0; v < V; ++v) sacc = fmaf((float)a[r][ch][v], (float)xv[ch][v], sacc);
+        dot[r] = (double)sacc;
+      }
+    }
+    {
+      const double tot = warp_multi_sum<R>(dot);
+      if ((lane & (32 / R - 1)) == 0) red[(buf * NW + warp) * R + warp_multi_row<R>(lane)] = tot;
+    }
+    named_bar_sync(1, NW * 32);
+    double* ybuf = red + 2 * NW * R;  // [2][R]
+    if (tid < R) {
+      double y = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) y += red[(buf * NW + w) * R + tid];
+      ybuf[buf * R + tid] = y;
+    }
+    named_bar_sync(1, NW * 32);
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double y = ybuf[buf * R + r];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[ch][v] = fma(y, (double)a[r][ch][v], acc[ch][v]);
+      }
+    } else {
+      // the R-row rank update in fp32, folded into the fp64 accumulator once per stage
+      float st[NCH][V];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int v = 0; v < V; ++v) st[ch][v] = 0.0f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float y = (float)ybuf[buf * R + r];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int v = 0; v < V; ++v) st[ch][v] = fmaf(y, (float)a[r][ch][v], st[ch][v]);
+      }
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[ch][v] += (double)st[ch][v];
+    }
+    buf ^= 1;
+  }
+  double* out = part + (int64_t)blockIdx.x * d;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    if (!act[ch]) continue;
+    const int64_t c = (int64_t)ch * (NW * 32) + tid;
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[c * V + v] = acc[ch][v];
+  }
+}
+
+template <typename T, int NCH, int R, int STAGES>
+static int launch_tma(adask_ctx* ctx, const T* A, int64_t n, int64_t d, int64_t lda, const double* x,
+                      double* part, int grid, cudaStream_t st) {
+  const size_t ring = align_up((size_t)STAGES * R * d * sizeof(T), 128);
+  const size_t smem = ring + 2 * STAGES * sizeof(uint64_t) + (2 * 8 * R + 2 * R) * sizeof(double);
+  auto kern = k_hess_tma<T, NCH, R, STAGES>;
+  ADASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, 288, smem, st>>>(A, n, d, lda, x, part);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
+// TMA path eligibility and dispatch: rows of 16-byte multiples, 16-byte
+// aligned base and pitch, d <= 256 * 8 chunks.  Stage = R rows ~ 32 KB.
+template <typename T>
+static int hess_partial_tma(adask_ctx* ctx, const T* A, int64_t n, int64_t d, int64_t lda,
+                            const double* x, double** part_out, int* nparts_out, cudaStream_t st,
+                            bool* used) {
+  constexpr int V = 16 / sizeof(T);
+  *used = false;
+  if ((uintptr_t)A % 16 || (d % V) || (lda * (int64_t)sizeof(T)) % 16) return ADASK_OK;
+  const int64_t nchunks = d / V;
+  int nch = (int)cdiv(nchunks, 256);
+  if (nch > 8) return ADASK_OK;
+  nch = nch <= 1 ? 1 : nch <= 2 ? 2 : nch <= 4 ? 4 : 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, cdiv(n, 16)));
+  void* wsp = nullptr;
+  ADASK_TRY(ctx->ws[WS_HESS].get((size_t)grid * d * sizeof(double), st, &wsp));
+  double* part = (double*)wsp;
+  *part_out = part;
+  *nparts_out = grid;
+  *used = true;
+  const int64_t row_bytes = d * (int64_t)sizeof(T);
+  switch (nch) {
+    case 1:
+      if (row_bytes <= 2048) return launch_tma<T, 1, 16, 6>(ctx, A, n, d, lda, x, part, grid, st);
+      return launch_tma<T, 1, 8, 6>(ctx, A, n, d, lda, x, part, grid, st);
+    case 2:
+      return launch_tma<T, 2, 4, 6>(ctx, A, n, d, lda, x, part, grid, st);
+    case 4:
+      return launch_tma<T, 4, 2, 6>(ctx, A, n, d, lda, x, part, grid, st);
+    default:
+      return launch_tma<T, 8, 1, 6>(ctx, A, n, d, lda, x, part, grid, st);
   }
 }
 
@@ -310,12 +527,19 @@ int hess_mult_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t 
       }
       continue;
     }
-    if (dtype == ADASK_F64)
-      ADASK_TRY(hess_partial<double>(ctx, (const double*)A, n, d, lda, x, &part, &nparts, st));
-    else if (dtype == ADASK_F32)
-      ADASK_TRY(hess_partial<float>(ctx, (const float*)A, n, d, lda, x, &part, &nparts, st));
-    else
+    bool used = false;
+    const bool tma_ok = getenv("ADASK_NO_TMA") == nullptr;
+    if (dtype == ADASK_F64) {
+      if (tma_ok)
+        ADASK_TRY(hess_partial_tma<double>(ctx, (const double*)A, n, d, lda, x, &part, &nparts, st, &used));
+      if (!used) ADASK_TRY(hess_partial<double>(ctx, (const double*)A, n, d, lda, x, &part, &nparts, st));
+    } else if (dtype == ADASK_F32) {
+      if (tma_ok)
+        ADASK_TRY(hess_partial_tma<float>(ctx, (const float*)A, n, d, lda, x, &part, &nparts, st, &used));
+      if (!used) ADASK_TRY(hess_partial<float>(ctx, (const float*)A, n, d, lda, x, &part, &nparts, st));
+    } else {
       return fail(ADASK_E_ARG, "bad dtype %d", dtype);
+    }
     k_hess_finish<<<(unsigned)cdiv(d, 32), 256, 0, st>>>(part, nparts, d, x, nu2, lam,
                                                          B ? B + j * ldb : nullptr,
                                                          out + j * ldo, partial ? 0 : 1);

@@ -79,6 +79,28 @@ __global__ void k_pcg_integers_norej(GenState g, uint64_t first, int64_t count, 
   for (int64_t i = i0; i < i1; ++i) out[i] = (OutT)lemire_value(s.next(), m);
 }
 
+// Sign bits of integers(0, 2, size=count) packed 32 per word (bit e of word w
+// = draw first + 32w + e; 1 -> +1).  m = 2 never rejects (Lemire threshold 0).
+__global__ void k_pcg_sign_bits(GenState g, uint64_t first, int64_t count, uint32_t* __restrict__ words) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = w * 32;
+  if (i0 >= count) return;
+  const int64_t n = count - i0 < 32 ? count - i0 : 32;
+  U32Stream s(g, first + (uint64_t)i0);
+  uint32_t bits = 0;
+  for (int e = 0; e < n; ++e) bits |= (lemire_value(s.next(), 2u) & 1u) << e;
+  words[w] = bits;
+}
+
+int pcg_sign_bits_impl(adask_ctx* ctx, const adask_pcg64* g, uint64_t first, int64_t count,
+                       uint32_t* words, cudaStream_t st) {
+  if (count <= 0) return ADASK_OK;
+  const int64_t nw = cdiv(count, 32);
+  k_pcg_sign_bits<<<(unsigned)cdiv(nw, 256), 256, 0, st>>>(GenState::from(*g), first, count, words);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
 int pcg_integers_impl(adask_ctx* ctx, const adask_pcg64* g, uint64_t first, int64_t item0,
                       int64_t count, int64_t total_items, uint32_t m, int32_t* out, uint64_t* next,
                       cudaStream_t st) {

@@ -100,4 +100,8 @@ int pcg_integers_impl(adask_ctx* ctx, const adask_pcg64* g, uint64_t first, int6
                       int64_t count, int64_t total_items, uint32_t m, int32_t* out, uint64_t* next,
                       cudaStream_t st);
 
+// Packed sign bits (bit = 1 -> +1) of integers(0, 2, size=count) from draw `first`.
+int pcg_sign_bits_impl(adask_ctx* ctx, const adask_pcg64* g, uint64_t first, int64_t count,
+                       uint32_t* words, cudaStream_t st);
+
 }  // namespace adask

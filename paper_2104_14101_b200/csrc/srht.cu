@@ -33,7 +33,7 @@ struct FwhtArgs {
   const void* src;
   int64_t src_ld;
   int64_t n_valid;  // rows >= n_valid read as zero (padding)
-  const int32_t* sgn;
+  const uint32_t* sgn;  // packed sign bits (bit = 1 -> +1), or null
   // pass 1 output: Z[(slot*G + blk) * d + c]; lo_to_slot null = identity
   const int32_t* lo_to_slot;
   void* Z;
@@ -137,8 +137,10 @@ __global__ void __launch_bounds__(256) k_fwht_tile(FwhtArgs a) {
   T* tile = reinterpret_cast<T*>(smem_raw);
   int* hi_to_k = reinterpret_cast<int*>(smem_raw + fw_tile_bytes<T, LOG>());
 
-  const int64_t blk = blockIdx.x;  // pass 1: row block; pass 2: slot
-  const int64_t c0 = (int64_t)blockIdx.y * C;
+  // column panels vary fastest across the grid so that concurrently running
+  // CTAs cover whole rows of A (DRAM page locality)
+  const int64_t blk = blockIdx.y;  // pass 1: row block; pass 2: slot
+  const int64_t c0 = (int64_t)blockIdx.x * C;
   const int64_t d = a.d;
 
   if constexpr (MODE == FW_P2) {
@@ -158,22 +160,27 @@ __global__ void __launch_bounds__(256) k_fwht_tile(FwhtArgs a) {
       const int c = u % C, q = u / C;
       const int64_t col = c0 + c;
       T v[E];
+      // rows q*E .. q*E + E - 1 (consecutive): all loads first, branch-free
+      const bool cok = col < d;
+      if constexpr (MODE == FW_P1) {
+        const int64_t g0 = blk * B + (int64_t)q * E;
+        const T* src = reinterpret_cast<const T*>(a.src) + (cok ? col : 0);
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int r = fw_row(q, e, 0, NB);
-        T x = (T)0;
-        if (col < d) {
-          if constexpr (MODE == FW_P1) {
-            const int64_t grow = blk * B + r;
-            if (grow < a.n_valid) {
-              x = reinterpret_cast<const T*>(a.src)[grow * a.src_ld + col];
-              if (a.sgn) x = a.sgn[grow] ? x : -x;  // diag(signs) A, exact
-            }
-          } else {
-            x = reinterpret_cast<const T*>(a.Z)[(blk * a.G + r) * d + col];
-          }
+        for (int e = 0; e < E; ++e) {
+          const int64_t grow = g0 + e;
+          const bool ok = cok && grow < a.n_valid;
+          v[e] = ok ? __ldg(src + (ok ? grow : 0) * a.src_ld) : (T)0;
         }
-        v[e] = x;
+        if (a.sgn) {
+          // diag(signs) A: exact negation where the sign bit is 0
+          const uint32_t bits = a.sgn[g0 >> 5] >> (g0 & 31);
+#pragma unroll
+          for (int e = 0; e < E; ++e) v[e] = ((bits >> e) & 1u) ? v[e] : -v[e];
+        }
+      } else {
+        const T* src = reinterpret_cast<const T*>(a.Z) + blk * a.G * d + (cok ? col : 0);
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = cok ? __ldg(src + (int64_t)(q * E + e) * d) : (T)0;
       }
       butterflies<T, NB>(v);
       if constexpr (Sh::ROUNDS == 1) {
@@ -247,7 +254,7 @@ static int launch_fw(adask_ctx* ctx, const FwhtArgs& a, int64_t nblk, cudaStream
   size_t smem = fw_tile_bytes<T, LOG>() + (MODE == FW_P2 ? sizeof(int) * (size_t)B : 0);
   auto kern = k_fwht_tile<T, LOG, MODE>;
   if (smem > 48 * 1024) ADASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)nblk, (unsigned)cdiv(a.d, C));
+  dim3 grid((unsigned)cdiv(a.d, C), (unsigned)nblk);
   kern<<<grid, 256, smem, st>>>(a);
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;
@@ -277,7 +284,7 @@ static int ilog2(int64_t n) {
 // over the slots, writing the requested rows.  idx = output row selection
 // (m entries, values in [0, n_pad)); idx == null means all n_pad rows in order.
 static int fwht_select(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
-                       const int32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m,
+                       const uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m,
                        void* out, int64_t ldo, double c1, double c2, int accumulate,
                        cudaStream_t st) {
   const int L = ilog2(n_pad);
@@ -385,9 +392,9 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4));
   // signs: draws [0, n) of integers(0, 2)
   void* sw = nullptr;
-  ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)n * 4, st, &sw));
-  int32_t* sgn = (int32_t*)sw;
-  ADASK_TRY(pcg_integers_impl(ctx, g, 0, 0, n, n, 2u, sgn, nullptr, st));
+  ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(n, 32) * 4 + 16, st, &sw));
+  uint32_t* sgn = (uint32_t*)sw;
+  ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
   // idx = choice(n_pad, m, replace=False) after the n sign draws (host)
   adask_pcg64 h = *g;
   adask_pcg64_skip_u32(&h, (uint64_t)n);

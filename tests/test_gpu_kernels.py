@@ -82,7 +82,8 @@ def test_hess_mult_fp32(ak, n, d):
     p = ak.RegularizedProblem(A, np.zeros(d), 0.5, dtype="float32")
     ref = O.Problem.make(A.astype(np.float64), np.zeros(d), 0.5).hess_mult(X)
     got = p.hess_mult(X)
-    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)  # fp64 accumulation of fp32 data
+    # fp32 data: per-thread partials in fp32, cross-thread reduction and accumulation in fp64
+    assert np.linalg.norm(got - ref) <= 2e-6 * np.linalg.norm(ref)
 
 
 @pytest.mark.parametrize("n,d,m,seed", [(64, 5, 16, 9), (1000, 37, 64, 3), (5000, 129, 1000, 4),
