@@ -241,7 +241,14 @@ int adask_cholesky(adask_ctx* ctx, int dtype, const void* M, int64_t k, int64_t 
 /* Fused iteration bodies (solvers.py:227-282 _PcgState, :522-546 _IhsState)*/
 /* ======================================================================== */
 
-/* Problem operand bundle for the iteration bodies. */
+/* In-place sum-all-reduce of `count` doubles across the ranks that share a
+ * row-sharded A (stream-ordered on `stream`); return 0 on success.  Supplied
+ * by the host runtime (NCCL through torch.distributed in the Python package). */
+typedef int (*adask_allreduce_fn)(double* buf, int64_t count, void* user, void* stream);
+
+/* Problem operand bundle for the iteration bodies.  A holds this rank's rows;
+ * with `allreduce` set, every H x is formed as all_reduce(A_local^T A_local x)
+ * + nu^2 Lam x (- B), i.e. one d*c all-reduce per loop pass.               */
 typedef struct adask_problem {
   int dtype;
   const void* A;
@@ -250,6 +257,8 @@ typedef struct adask_problem {
   double nu2;         /* nu^2 */
   const double* lam;  /* device, d        */
   const double* B;    /* device, c x d    */
+  adask_allreduce_fn allreduce; /* null on one GPU */
+  void* allreduce_user;
 } adask_problem;
 
 /* _PcgState.restart (solvers.py:243-248): r = B - H x; rt = P^-1 r;

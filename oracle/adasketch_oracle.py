@@ -121,6 +121,19 @@ def sjlt_sequential(A: np.ndarray, m: int, seed: int) -> np.ndarray:
     return SA
 
 
+def sjlt_shard(A_local: np.ndarray, m: int, seed: int, row0: int, n_total: int) -> np.ndarray:
+    """Partial SJLT sketch of global rows [row0, row0 + n_local): buckets and
+    signs are the reference's draws for those global rows (embeddings.py:
+    117-124 over the full n_total), summed in ascending row order."""
+    A_local = np.asarray(A_local, dtype=np.float64)
+    rows, bits = sjlt_draws(n_total, m, seed, 1)
+    SA = np.zeros((m, A_local.shape[1]))
+    for i in range(A_local.shape[0]):
+        g = row0 + i
+        SA[rows[g]] += A_local[i] if bits[g] else -A_local[i]
+    return SA
+
+
 def philox4x32_10(ctr: np.ndarray, key: tuple[int, int]) -> np.ndarray:
     """Philox4x32-10 on a (..., 4) uint32 counter array (Salmon et al. 2011)."""
     M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
@@ -174,6 +187,15 @@ def sketch_gaussian(A: np.ndarray, m: int, seed: int, S: np.ndarray | None = Non
     A = np.asarray(A, dtype=np.float64)
     if S is None:
         S = philox_gaussian(m, A.shape[0], seed)
+    return S @ A
+
+
+def numpy_gaussian(A: np.ndarray, m: int, seed: int) -> np.ndarray:
+    """The reference's own Gaussian sketch (embeddings.py:66-73: ziggurat
+    normals from default_rng(seed), divided by sqrt(m)); used to pin the
+    oracle's driver against the reference's traces."""
+    A = np.asarray(A, dtype=np.float64)
+    S = np.random.default_rng(seed).standard_normal((m, A.shape[0])) / np.sqrt(m)
     return S @ A
 
 

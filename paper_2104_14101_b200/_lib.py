@@ -46,6 +46,9 @@ class PCG64State(C.Structure):
     ]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
 class Problem(C.Structure):
     _fields_ = [
         ("dtype", C.c_int),
@@ -57,6 +60,8 @@ class Problem(C.Structure):
         ("nu2", C.c_double),
         ("lam", C.c_void_p),
         ("B", C.c_void_p),
+        ("allreduce", ALLREDUCE_FN),
+        ("allreduce_user", C.c_void_p),
     ]
 
 
@@ -123,7 +128,7 @@ def lib():
                 if not LIB_PATH.exists():
                     raise ImportError(
                         f"{LIB_PATH} is missing: build it with "
-                        "`python -m paper_2104_14101_b200.build` (there is no CPU fallback)"
+                        "`python -m paper_2104_14101_b200.buildlib` (there is no CPU fallback)"
                     )
                 h = C.CDLL(str(LIB_PATH))
                 for name, (res, args) in _PROTOS.items():

@@ -1,6 +1,6 @@
 """Build libadask.so in-tree with nvcc for sm_100a.
 
-    python -m paper_2104_14101_b200.build [--verbose] [--force]
+    python -m paper_2104_14101_b200.buildlib [--verbose] [--force]
 
 Every translation unit under csrc/ is compiled with
 `-gencode arch=compute_100a,code=sm_100a -lineinfo -O3` and linked into

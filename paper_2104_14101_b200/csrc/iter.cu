@@ -167,6 +167,21 @@ static int read_scalars(adask_ctx* ctx, IterScalars* sc, double* dt_host, int* f
   return ADASK_OK;
 }
 
+// H X (- B) for the problem; row-sharded problems all-reduce the partial
+// A_local^T A_local X before the regularizer / B epilogue.
+static int problem_hess(adask_ctx* ctx, const adask_problem* pb, const double* X, const double* B,
+                        double* out, cudaStream_t st) {
+  const int64_t d = pb->d, c = pb->c;
+  if (!pb->allreduce)
+    return hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, X, c, d, pb->nu2, pb->lam, B, d, out,
+                          d, 0, st);
+  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, X, c, d, pb->nu2, pb->lam, nullptr, d,
+                           out, d, ADASK_PARTIAL, st));
+  if (pb->allreduce(out, d * c, pb->allreduce_user, (void*)st) != 0)
+    return fail(ADASK_E_CUDA, "all-reduce of the partial A^T A x failed");
+  return vec_hess_finish_impl(ctx, out, d, c, d, X, pb->nu2, pb->lam, B, out, st);
+}
+
 static int check_problem(const adask_problem* pb) {
   if (!pb || !pb->A || pb->n < 0 || pb->d < 1 || pb->c < 1 || pb->lda < pb->d || !pb->lam)
     return fail(ADASK_E_ARG, "bad problem descriptor");
@@ -185,8 +200,7 @@ extern "C" int adask_pcg_restart(adask_ctx* ctx, const adask_problem* pb, const 
   cudaStream_t st = S(stream);
   const int64_t d = pb->d, c = pb->c;
   // r = B - H x   (computed as -(H x - B), exact)
-  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, x, c, d, pb->nu2, pb->lam, pb->B,
-                           d, r, d, 0, st));
+  ADASK_TRY(problem_hess(ctx, pb, x, pb->B, r, st));
   k_negate<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(r, d * c);
   ADASK_LAUNCHED(ctx);
   ADASK_TRY(precond_apply_impl(ctx, P, r, c, d, rt, d, st));
@@ -209,8 +223,7 @@ extern "C" int adask_pcg_propose(adask_ctx* ctx, const adask_problem* pb, const 
   ADASK_TRY(check_problem(pb));
   cudaStream_t st = S(stream);
   const int64_t d = pb->d, c = pb->c;
-  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, c, d, pb->nu2, pb->lam,
-                           nullptr, d, Hp, d, 0, st));
+  ADASK_TRY(problem_hess(ctx, pb, p, nullptr, Hp, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
   k_pcg_step<<<1, kVecThreads, 0, st>>>(d, c, x, r, p, Hp, dt_col, x_new, r_new, sc);
@@ -241,8 +254,7 @@ extern "C" int adask_ihs_restart(adask_ctx* ctx, const adask_problem* pb, const 
   ADASK_TRY(check_problem(pb));
   cudaStream_t st = S(stream);
   const int64_t d = pb->d, c = pb->c;
-  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, x, c, d, pb->nu2, pb->lam, pb->B,
-                           d, g, d, 0, st));
+  ADASK_TRY(problem_hess(ctx, pb, x, pb->B, g, st));
   ADASK_TRY(precond_apply_impl(ctx, P, g, c, d, v, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
@@ -262,8 +274,7 @@ extern "C" int adask_ihs_propose(adask_ctx* ctx, const adask_problem* pb, const 
   const int64_t d = pb->d, c = pb->c;
   k_ihs_step<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(d * c, x, v, mu, x_prev, beta, x_new);
   ADASK_LAUNCHED(ctx);
-  ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, x_new, c, d, pb->nu2, pb->lam,
-                           pb->B, d, g_new, d, 0, st));
+  ADASK_TRY(problem_hess(ctx, pb, x_new, pb->B, g_new, st));
   ADASK_TRY(precond_apply_impl(ctx, P, g_new, c, d, v_new, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));

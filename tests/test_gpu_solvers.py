@@ -68,3 +68,51 @@ def test_direct_solve_and_exact_error():
     e = ak.exact_error(p, x, ak.ExactSolution(xso))
     eo = O.exact_error(po, x, xso)
     assert abs(e - eo) <= 1e-12 * abs(eo)
+
+
+def test_block_srht_sketcher_bitwise():
+    import torch
+
+    import paper_2104_14101_b200 as ak
+    from paper_2104_14101_b200.embeddings import SketchSpec
+    from paper_2104_14101_b200.parallel import block_srht_sketcher
+
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((5 * 512 + 100, 6))
+    p = ak.RegularizedProblem(A, np.zeros(6), 0.1)
+    SA = block_srht_sketcher(512)(p, SketchSpec("srht-block", 64, 77)).cpu().numpy()
+    assert np.array_equal(SA, O.block_srht(A, 64, 77, 512))
+
+
+def test_sharded_problem_allreduce_hook_world1():
+    """The allreduce hook inside the fused iteration bodies (NCCL, world 1):
+    same schedule and x as the unsharded solver."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_14101_b200 as ak
+    from paper_2104_14101_b200.parallel import Comm, ShardedProblem, shard_rows, sharded_sketcher
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(s.getsockname()[1]))
+    s.close()
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        j = np.arange(1, 129, dtype=float)
+        A, b, lam = _instance(1 << 13, 128, j**-0.5, 1e-3, True)
+        comm = Comm()
+        comm.world = 2  # force the exchange path (all-reduce over the single rank)
+        plan = shard_rows(A.shape[0], 1, 0)
+        ps = ShardedProblem(A, b, 1e-3, lam, plan=plan, comm=comm)
+        cfg = ak.AdaptiveConfig.for_method("pcg", 0.125, 8, 8, "sjlt", 1)
+        x, tr = ak.adaptive_run(ps, np.zeros(128), cfg, sketcher=sharded_sketcher(comm))
+        p = ak.RegularizedProblem(A, b, 1e-3, lam)
+        x1, tr1 = ak.adaptive_run(p, np.zeros(128), cfg)
+        assert _events(tr) == _events(tr1)
+        assert np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
+    finally:
+        dist.destroy_process_group()
