@@ -241,10 +241,10 @@ int adask_cholesky(adask_ctx* ctx, int dtype, const void* M, int64_t k, int64_t 
 /* Fused iteration bodies (solvers.py:227-282 _PcgState, :522-546 _IhsState)*/
 /* ======================================================================== */
 
-/* In-place sum-all-reduce of `count` doubles across the ranks that share a
+/* In-place sum-all-reduce of `count` elements (dtype ADASK_F64 / ADASK_F32) across the ranks that share a
  * row-sharded A (stream-ordered on `stream`); return 0 on success.  Supplied
  * by the host runtime (NCCL through torch.distributed in the Python package). */
-typedef int (*adask_allreduce_fn)(double* buf, int64_t count, void* user, void* stream);
+typedef int (*adask_allreduce_fn)(void* buf, int64_t count, int dtype, void* user, void* stream);
 
 /* Problem operand bundle for the iteration bodies.  A holds this rank's rows;
  * with `allreduce` set, every H x is formed as all_reduce(A_local^T A_local x)
@@ -289,6 +289,44 @@ int adask_ihs_propose(adask_ctx* ctx, const adask_problem* pb, const adask_preco
                       const double* x, const double* v, double mu, const double* x_prev,
                       double beta, double* x_new, double* g_new, double* v_new,
                       double* delta_tilde_host, void* stream);
+
+/* ======================================================================== */
+/* Native adaptive driver (solvers.py:585-659)                              */
+/* ======================================================================== */
+enum { ADASK_METHOD_IHS = 0, ADASK_METHOD_PCG = 1, ADASK_METHOD_POLYAK = 2 };
+enum { ADASK_GAUSSIAN = 0, ADASK_SRHT = 1, ADASK_SJLT = 2, ADASK_SRHT_BLOCK = 3 };
+enum { ADASK_EV_PLAIN = 0, ADASK_EV_ACCEPTED = 1, ADASK_EV_RESKETCH = 2 };
+
+/* AdaptiveConfig (solvers.py:465-519) plus the B200 extras. */
+typedef struct adask_adaptive_cfg {
+  int method;            /* ADASK_METHOD_*                                   */
+  int family;            /* ADASK_GAUSSIAN / SRHT / SJLT / SRHT_BLOCK        */
+  double rho;
+  int64_t m_init, T;
+  uint64_t seed;         /* base seed; resketch K uses derive_seed(seed, K)  */
+  int64_t s;             /* SJLT nonzeros per column                         */
+  double alpha, phi_rho, c_alpha_rho;
+  int64_t block;         /* block-SRHT rows per block                        */
+  int64_t row0, n_total; /* this rank's first global row, global row count   */
+  uint32_t flags;        /* ADASK_TF32                                       */
+} adask_adaptive_cfg;
+
+/* TraceRecord (solvers.py:51-59). */
+typedef struct adask_trace_rec {
+  int64_t t, m, k;
+  double delta_tilde;
+  double delta_exact;    /* valid when has_exact */
+  double wall_seconds;
+  int32_t event;         /* ADASK_EV_*           */
+  int32_t has_exact;
+} adask_trace_rec;
+
+/* adaptive_run: x0 / x_out are c columns of length d (device); xstar
+ * (nullable, device) enables the exact error of every record.  recs needs
+ * room for 3*T + 64 records.                                              */
+int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const adask_adaptive_cfg* cfg,
+                       const double* x0, double* x_out, const double* xstar, adask_trace_rec* recs,
+                       int64_t max_recs, int64_t* n_recs, void* stream);
 
 /* 0.5 * sum(a .* b) over c columns of length d (deterministic). */
 int adask_dot(adask_ctx* ctx, const double* a, const double* b, int64_t d, int64_t c,

@@ -46,7 +46,7 @@ class PCG64State(C.Structure):
     ]
 
 
-ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p)
 
 
 class Problem(C.Structure):
@@ -62,6 +62,38 @@ class Problem(C.Structure):
         ("B", C.c_void_p),
         ("allreduce", ALLREDUCE_FN),
         ("allreduce_user", C.c_void_p),
+    ]
+
+
+class AdaptiveCfg(C.Structure):
+    _fields_ = [
+        ("method", C.c_int),
+        ("family", C.c_int),
+        ("rho", C.c_double),
+        ("m_init", C.c_int64),
+        ("T", C.c_int64),
+        ("seed", C.c_uint64),
+        ("s", C.c_int64),
+        ("alpha", C.c_double),
+        ("phi_rho", C.c_double),
+        ("c_alpha_rho", C.c_double),
+        ("block", C.c_int64),
+        ("row0", C.c_int64),
+        ("n_total", C.c_int64),
+        ("flags", C.c_uint32),
+    ]
+
+
+class TraceRec(C.Structure):
+    _fields_ = [
+        ("t", C.c_int64),
+        ("m", C.c_int64),
+        ("k", C.c_int64),
+        ("delta_tilde", C.c_double),
+        ("delta_exact", C.c_double),
+        ("wall_seconds", C.c_double),
+        ("event", C.c_int32),
+        ("has_exact", C.c_int32),
     ]
 
 
@@ -112,6 +144,7 @@ _PROTOS = {
     "adask_ihs_restart": (C.c_int, [vp, P(Problem), vp, vp, vp, vp, P(dbl), vp]),
     "adask_ihs_propose": (C.c_int, [vp, P(Problem), vp, vp, vp, dbl, vp, dbl, vp, vp, vp, P(dbl), vp]),
     "adask_dot": (C.c_int, [vp, vp, vp, i64, i64, i64, P(dbl), vp]),
+    "adask_adaptive_run": (C.c_int, [vp, P(Problem), P(AdaptiveCfg), vp, vp, vp, P(TraceRec), i64, P(i64), vp]),
 }
 
 _lib = None

@@ -1,0 +1,276 @@
+// Native adaptive driver: adaptive_run (solvers.py:585-659) in C++.
+//
+// The accept / reject control flow, the thresholds c(alpha, rho) phi^ell
+// (pow on doubles, as Python's float ** int), the converged floor, the cap and
+// capped-retry rules and the derive_seed(seed, K) redraw chain follow the
+// reference statement by statement; the Python implementation in solvers.py
+// is the same logic and the tests compare both traces.  Running the loop
+// natively removes the Python/ctypes round trips around every loop pass: what
+// remains per pass is the device work plus one 64-byte readback of the new
+// decrement.  Sketches (all families, row-sharded with global randomness),
+// the preconditioner build and the fused iteration bodies are the libadask
+// kernels; sharded problems all-reduce SA and A^T A x through the problem's
+// allreduce hook.
+#include <chrono>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "hessmult.cuh"
+#include "precond.cuh"
+#include "rng.cuh"
+#include "sjlt.cuh"
+#include "srht.cuh"
+
+namespace adask {
+int problem_hess(adask_ctx* ctx, const adask_problem* pb, const double* X, const double* B, double* out,
+                 cudaStream_t st);
+
+__global__ void k_sub(int64_t n, const double* a, const double* b, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] - b[i];
+}
+
+static void seed_words(uint64_t v, std::vector<uint32_t>& w) {
+  w.clear();
+  do {
+    w.push_back((uint32_t)v);
+    v >>= 32;
+  } while (v);
+}
+
+static int gen_from_seed(uint64_t seed, adask_pcg64* g) {
+  std::vector<uint32_t> w;
+  seed_words(seed, w);
+  return adask_pcg64_seed(w.data(), (int64_t)w.size(), g);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  int alloc(size_t bytes, cudaStream_t s) {
+    st = s;
+    ADASK_CUDA(cudaMallocAsync(&p, bytes ? bytes : 16, s));
+    return ADASK_OK;
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+// SA (m x d, dtype) for the configured family at sketch seed `seed`.
+static int make_sketch(adask_ctx* ctx, const adask_problem* pb, const adask_adaptive_cfg* cfg, int64_t m,
+                       uint64_t seed, void* SA, cudaStream_t st) {
+  const int64_t d = pb->d;
+  const size_t esz = pb->dtype == ADASK_F64 ? 8 : 4;
+  switch (cfg->family) {
+    case ADASK_GAUSSIAN:
+      ADASK_TRY(adask_sketch_gaussian(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, cfg->row0, m, seed, SA, d,
+                                      cfg->flags & ADASK_TF32, (void*)st));
+      break;
+    case ADASK_SRHT: {
+      if (cfg->n_total != pb->n) return fail(ADASK_E_ARG, "the global SRHT does not shard (use block SRHT)");
+      adask_pcg64 g;
+      ADASK_TRY(gen_from_seed(seed, &g));
+      ADASK_TRY(sketch_srht_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, &g, m, SA, d, nullptr, 0, st));
+      break;
+    }
+    case ADASK_SRHT_BLOCK: {
+      const int64_t B = cfg->block;
+      if (B < 1 || cfg->row0 % B) return fail(ADASK_E_ARG, "block SRHT: shard must start on a block boundary");
+      ADASK_CUDA(cudaMemsetAsync(SA, 0, (size_t)m * d * esz, st));
+      for (int64_t r0 = 0; r0 < pb->n; r0 += B) {
+        const int64_t rows = std::min<int64_t>(B, pb->n - r0);
+        adask_pcg64 g;
+        ADASK_TRY(gen_from_seed(adask_derive_seed(seed, (uint64_t)((cfg->row0 + r0) / B)), &g));
+        const void* Ab = (const char*)pb->A + (size_t)r0 * pb->lda * esz;
+        ADASK_TRY(sketch_srht_impl(ctx, pb->dtype, Ab, rows, d, pb->lda, &g, m, SA, d, nullptr,
+                                   ADASK_ACCUMULATE, st));
+      }
+      break;
+    }
+    case ADASK_SJLT: {
+      adask_pcg64 g;
+      ADASK_TRY(gen_from_seed(seed, &g));
+      std::vector<int64_t> rows;
+      uint64_t sign_first = 0;
+      if (cfg->s > 1) {
+        if (cfg->row0 != 0 || cfg->n_total != pb->n)
+          return fail(ADASK_E_ARG, "row-sharded SJLT with s > 1 is not supported");
+        rows.resize((size_t)(pb->n * cfg->s));
+        adask_pcg64 h = g;
+        ADASK_TRY(adask_sjlt_rows(&h, pb->n, m, cfg->s, rows.data(), &sign_first));
+      }
+      ADASK_TRY(sketch_sjlt_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, cfg->row0, cfg->n_total, m,
+                                 cfg->s, &g, rows.empty() ? nullptr : rows.data(), sign_first, SA, d, 0, st));
+      break;
+    }
+    default:
+      return fail(ADASK_E_ARG, "unknown sketch family %d", cfg->family);
+  }
+  if (pb->allreduce && pb->allreduce(SA, m * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
+    return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
+  return ADASK_OK;
+}
+
+static int exact_err(adask_ctx* ctx, const adask_problem* pb, const double* x, const double* xstar,
+                     double* diff, double* Hd, double* out, cudaStream_t st) {
+  const int64_t n = pb->d * pb->c;
+  k_sub<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, x, xstar, diff);
+  ADASK_LAUNCHED(ctx);
+  ADASK_TRY(problem_hess(ctx, pb, diff, nullptr, Hd, st));
+  return adask_dot(ctx, diff, Hd, pb->d, pb->c, pb->d, out, (void*)st);
+}
+
+}  // namespace adask
+
+using namespace adask;
+
+extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const adask_adaptive_cfg* cfg,
+                                  const double* x0, double* x_out, const double* xstar,
+                                  adask_trace_rec* recs, int64_t max_recs, int64_t* n_recs, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (!pb || !cfg || !x0 || !x_out || !recs || !n_recs) return fail(ADASK_E_ARG, "adaptive_run: null argument");
+  if (!(cfg->rho > 0.0 && cfg->rho < 1.0)) return fail(ADASK_E_ARG, "rho must lie in (0, 1)");
+  if (cfg->m_init < 1 || cfg->T < 0) return fail(ADASK_E_ARG, "bad m_init / T");
+  cudaStream_t st = S(stream);
+  const auto t_start = std::chrono::steady_clock::now();
+  auto wall = [&]() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  };
+  const int64_t d = pb->d, c = pb->c, cd = c * d;
+  const size_t esz = pb->dtype == ADASK_F64 ? 8 : 4;
+  *n_recs = 0;
+  // state buffers
+  DevBuf vecs;
+  ADASK_TRY(vecs.alloc((size_t)(12 * cd + 4 * c) * sizeof(double), st));
+  double* base = (double*)vecs.p;
+  double *x = base, *xn = base + cd, *a1 = base + 2 * cd, *a2 = base + 3 * cd, *a3 = base + 4 * cd;
+  double *b1 = base + 5 * cd, *b2 = base + 6 * cd, *b3 = base + 7 * cd, *xp = base + 8 * cd;
+  double *diff = base + 9 * cd, *Hd = base + 10 * cd, *Hp = base + 11 * cd;
+  double *dtc = base + 12 * cd, *dtn = dtc + c;  // per-column r.rt (current / proposed)
+  ADASK_CUDA(cudaMemcpyAsync(x, x0, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
+
+  const int64_t n_pad_total = (int64_t)1 << (int)std::ceil(std::log2((double)std::max<int64_t>(cfg->n_total, 1)));
+  int64_t cap = cfg->family == ADASK_SRHT ? n_pad_total : cfg->n_total;
+  if (cfg->family == ADASK_SRHT_BLOCK) {
+    // each block sketch needs m <= padded block rows
+    const int64_t b = std::min(cfg->block, cfg->n_total);
+    const int64_t bpad = (int64_t)1 << (int)std::ceil(std::log2((double)std::max<int64_t>(b, 1)));
+    cap = std::min(cap, bpad);
+  }
+  int64_t m = std::min(cfg->m_init, cap);
+  int64_t K = 0;
+  auto record = [&](int64_t t, int64_t mm, int64_t k, double dt, const double* xs, int ev) -> int {
+    if (*n_recs >= max_recs) return fail(ADASK_E_ARG, "trace buffer too small");
+    adask_trace_rec& r = recs[*n_recs];
+    r.t = t;
+    r.m = mm;
+    r.k = k;
+    r.delta_tilde = dt;
+    r.delta_exact = NAN;
+    r.has_exact = 0;
+    if (xstar) {
+      ADASK_TRY(exact_err(ctx, pb, xs, xstar, diff, Hd, &r.delta_exact, st));
+      r.has_exact = 1;
+    }
+    r.wall_seconds = wall();
+    r.event = ev;
+    ++*n_recs;
+    return ADASK_OK;
+  };
+
+  // sketch + build
+  DevBuf sa_buf;
+  ADASK_TRY(sa_buf.alloc((size_t)m * d * esz, st));
+  ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, 0), sa_buf.p, st));
+  adask_precond* P = nullptr;
+  int64_t info = 0;
+  ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
+                                (void*)st));
+  struct PGuard {
+    adask_precond** p;
+    ~PGuard() {
+      if (*p) adask_precond_destroy(*p);
+    }
+  } pguard{&P};
+
+  const bool pcg = cfg->method == ADASK_METHOD_PCG;
+  const bool polyak = cfg->method == ADASK_METHOD_POLYAK;
+  double mu = 1.0 - cfg->rho, beta = 0.0;
+  if (polyak) {
+    const double root = std::sqrt(1.0 - cfg->rho);
+    mu = 2.0 * (1.0 - cfg->rho) / (1.0 + root);
+    beta = (1.0 - root) / (1.0 + root);
+  }
+  // PCG: a1 = r, a2 = rt, a3 = p ; b1 = r_new, b2 = rt_new ; IHS: a1 = g, a2 = v, b1 = g_new, b2 = v_new
+  double delta = 0.0;
+  auto restart = [&]() -> int {
+    if (pcg) return adask_pcg_restart(ctx, pb, P, x, a1, a2, a3, dtc, &delta, (void*)st);
+    ADASK_TRY(adask_ihs_restart(ctx, pb, P, x, a1, a2, &delta, (void*)st));
+    if (polyak) ADASK_CUDA(cudaMemcpyAsync(xp, x, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return ADASK_OK;
+  };
+  ADASK_TRY(restart());
+  const double dt_first = delta;
+  double dt_I = delta;
+  int64_t t = 0, I = 0;
+  bool capped_retry = false;
+  ADASK_TRY(record(0, m, 0, delta, x, ADASK_EV_PLAIN));
+  while (t < cfg->T) {
+    double dnew = 0.0;
+    if (pcg)
+      ADASK_TRY(adask_pcg_propose(ctx, pb, P, x, a1, a3, dtc, Hp, xn, b1, b2, dtn, &dnew, (void*)st));
+    else
+      ADASK_TRY(adask_ihs_propose(ctx, pb, P, x, a2, mu, polyak ? xp : nullptr, beta, xn, b1, b2, &dnew,
+                                  (void*)st));
+    const int64_t ell = t + 1 - I;
+    const double threshold = cfg->c_alpha_rho * std::pow(cfg->phi_rho, (double)ell);
+    const bool converged = dt_I <= 0.0 || dnew <= 1e-26 * dt_first;
+    bool reject = (!converged) && dnew > threshold * dt_I;
+    if (reject && capped_retry) reject = false;  // m already at cap and one redraw failed: accept
+    if (reject) {
+      K += 1;
+      const bool at_cap = m >= cap;
+      m = std::min(2 * m, cap);
+      capped_retry = at_cap;
+      adask_precond_destroy(P);
+      P = nullptr;
+      DevBuf nsa;
+      ADASK_TRY(nsa.alloc((size_t)m * d * esz, st));
+      ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, (uint64_t)K), nsa.p, st));
+      std::swap(sa_buf.p, nsa.p);  // the previous SA is released (stream-ordered) with nsa
+      ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
+                                    (void*)st));
+      ADASK_TRY(restart());
+      dt_I = delta;
+      I = t;
+      ADASK_TRY(record(t, m, K, dt_I, x, ADASK_EV_RESKETCH));
+    } else {
+      if (pcg) {
+        // commit: p = rt_new + p * (dt_new / dt_old), then rotate the buffers
+        ADASK_TRY(adask_pcg_commit(ctx, d, c, b2, dtn, dtc, a3, (void*)st));
+        std::swap(x, xn);
+        std::swap(a1, b1);
+        std::swap(a2, b2);
+        std::swap(dtc, dtn);
+      } else {
+        if (polyak) {
+          std::swap(xp, x);  // x_prev <- x
+          std::swap(x, xn);  // x <- x_new (xn now holds the stale x_prev: scratch)
+        } else {
+          std::swap(x, xn);
+        }
+        std::swap(a1, b1);
+        std::swap(a2, b2);
+      }
+      delta = dnew;
+      t += 1;
+      capped_retry = false;
+      ADASK_TRY(record(t, m, K, delta, x, ADASK_EV_ACCEPTED));
+    }
+  }
+  ADASK_CUDA(cudaMemcpyAsync(x_out, x, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  ADASK_CUDA(cudaStreamSynchronize(st));
+  return ADASK_OK;
+}

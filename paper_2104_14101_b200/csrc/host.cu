@@ -341,6 +341,14 @@ int adask_ctx_create(int device, adask_ctx** out) {
   }
   if (device < 0 || device >= n) return fail(ADASK_E_ARG, "device %d out of range", device);
   ADASK_CUDA(cudaSetDevice(device));
+  // Keep freed stream-ordered allocations in the device's default pool (the
+  // solver allocates and frees preconditioners / sketches every resketch).
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
   adask_ctx* c = new adask_ctx();
   c->device = device;
   e = cudaMallocHost(&c->pinned, 64 * sizeof(double));

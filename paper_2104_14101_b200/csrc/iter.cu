@@ -169,7 +169,7 @@ static int read_scalars(adask_ctx* ctx, IterScalars* sc, double* dt_host, int* f
 
 // H X (- B) for the problem; row-sharded problems all-reduce the partial
 // A_local^T A_local X before the regularizer / B epilogue.
-static int problem_hess(adask_ctx* ctx, const adask_problem* pb, const double* X, const double* B,
+int problem_hess(adask_ctx* ctx, const adask_problem* pb, const double* X, const double* B,
                         double* out, cudaStream_t st) {
   const int64_t d = pb->d, c = pb->c;
   if (!pb->allreduce)
@@ -177,7 +177,7 @@ static int problem_hess(adask_ctx* ctx, const adask_problem* pb, const double* X
                           d, 0, st);
   ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, X, c, d, pb->nu2, pb->lam, nullptr, d,
                            out, d, ADASK_PARTIAL, st));
-  if (pb->allreduce(out, d * c, pb->allreduce_user, (void*)st) != 0)
+  if (pb->allreduce(out, d * c, ADASK_F64, pb->allreduce_user, (void*)st) != 0)
     return fail(ADASK_E_CUDA, "all-reduce of the partial A^T A x failed");
   return vec_hess_finish_impl(ctx, out, d, c, d, X, pb->nu2, pb->lam, B, out, st);
 }

@@ -78,9 +78,9 @@ class _CudaView:
     """__cuda_array_interface__ wrapper so a raw device pointer handed to the
     allreduce hook becomes a torch tensor without a copy."""
 
-    def __init__(self, ptr: int, count: int):
-        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
-                                         "version": 3, "strides": None}
+    def __init__(self, ptr: int, count: int, dtype: int = _lib.F64):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8" if dtype == _lib.F64 else "<f4",
+                                         "data": (ptr, False), "version": 3, "strides": None}
 
 
 class ShardedProblem(RegularizedProblem):
@@ -92,9 +92,9 @@ class ShardedProblem(RegularizedProblem):
         self.plan = plan
         self.comm = comm
 
-        def _hook(ptr, count, user, stream):
+        def _hook(ptr, count, dtype, user, stream):
             try:
-                t = torch.as_tensor(_CudaView(int(ptr), int(count)), device=self.A.device)
+                t = torch.as_tensor(_CudaView(int(ptr), int(count), int(dtype)), device=self.A.device)
                 self.comm.all_reduce_sum_(t)
                 return 0
             except Exception:  # reported through the C status path

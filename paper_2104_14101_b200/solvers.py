@@ -13,6 +13,7 @@ decrement).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -409,20 +410,68 @@ def _adaptive_sketch(p: RegularizedProblem, cfg: AdaptiveConfig, m: int, K: int,
     return sketch_dev(p.A, spec, tf32=tf32)
 
 
+_FAMILY_CODE = {"gaussian": 0, "srht": 1, "sjlt": 2, "srht-block": 3}
+_EVENTS = ("plain", "accepted", "resketch")
+
+
+def _adaptive_native(p: RegularizedProblem, x0, cfg: AdaptiveConfig, method: str, sol, tf32: bool,
+                     block: int):
+    """The same algorithm as the Python loop below, run by libadask's native
+    driver (adask_adaptive_run): no Python / ctypes round trips per pass."""
+    Xt, vec = _promote(p, x0)
+    xout = torch.empty_like(Xt)
+    c = _lib.AdaptiveCfg()
+    c.method = _METHODS.index(method)
+    c.family = _FAMILY_CODE[cfg.family]
+    c.rho, c.m_init, c.T, c.seed, c.s = float(cfg.rho), int(cfg.m_init), int(cfg.T), int(cfg.seed), int(cfg.s)
+    c.alpha, c.phi_rho, c.c_alpha_rho = float(cfg.alpha), float(cfg.phi_rho), float(cfg.c_alpha_rho)
+    c.block, c.row0, c.n_total = int(block), int(p.row0), int(p.n_total)
+    c.flags = _lib.TF32 if tf32 else 0
+    if method == "polyak":
+        c.phi_rho = 0.0  # the polyak threshold is evaluated on the host (see below)
+    nmax = 3 * int(cfg.T) + 200
+    recs = (_lib.TraceRec * nmax)()
+    nrec = C.c_int64()
+    xs = _sol_cols(sol)
+    pb = p.descriptor()
+    _lib.check(_lib.lib().adask_adaptive_run(dv.ctx().handle, C.byref(pb), C.byref(c), Xt.data_ptr(),
+                                             xout.data_ptr(), None if xs is None else xs.data_ptr(), recs,
+                                             nmax, C.byref(nrec), dv.stream()), "adaptive_run")
+    trace = SolverTrace()
+    for r in recs[:nrec.value]:
+        trace.append(TraceRecord(int(r.t), int(r.m), int(r.k), float(r.delta_tilde),
+                                 float(r.delta_exact) if r.has_exact else None, float(r.wall_seconds),
+                                 _EVENTS[r.event]))
+    return dv.from_columns(xout, vec, x0), trace
+
+
 def adaptive_run(p: RegularizedProblem, x0, cfg: AdaptiveConfig, method: str = "pcg",
                  sol: ExactSolution | None = None, experimental: bool = False, *,
-                 tf32: bool = False, sketcher=None):
+                 tf32: bool = False, sketcher=None, block: int = 1 << 21, native: bool | None = None):
     """Run a sketched method with on-line sketch-size adaptation
     (solvers.py:585-659).  Keyword-only extras: tf32 (fp32 Gaussian sketch on
-    tensor cores) and sketcher(p, spec) -> SA device tensor (e.g. the
-    block-SRHT of parallel.block_srht_sketcher)."""
+    tensor cores), block (rows per block for family "srht-block", config 4),
+    sketcher(p, spec) -> SA device tensor (custom sketches; forces the Python
+    loop), native (default: the libadask driver whenever no custom sketcher
+    is given; set ADASK_PY_DRIVER=1 to force the Python loop)."""
     if method not in _METHODS:
         raise ValueError(f"unknown method {method!r}; expected one of {_METHODS}")
     if method == "polyak" and not experimental:
         raise ValueError("method 'polyak' is experimental; pass experimental=True")
+    if native is None:
+        native = (sketcher is None and method != "polyak" and 0 <= int(cfg.seed) < 2**64
+                  and cfg.family in _FAMILY_CODE and os.environ.get("ADASK_PY_DRIVER") != "1")
+    if native:
+        return _adaptive_native(p, x0, cfg, method, sol, tf32, block)
+    if sketcher is None and cfg.family == "srht-block":
+        from .parallel import block_srht_sketcher
+
+        sketcher = block_srht_sketcher(block)
     clock = _Clock()
     Xt, vec = _promote(p, x0)
     cap = padded_rows(p.n_total) if cfg.family == "srht" else p.n_total
+    if cfg.family == "srht-block":
+        cap = min(cap, padded_rows(min(block, p.n_total)))  # each block sketch needs m <= padded rows
     m = min(cfg.m_init, cap)
     K = 0
     SA = _adaptive_sketch(p, cfg, m, K, sketcher, tf32)

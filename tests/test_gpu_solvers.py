@@ -116,3 +116,22 @@ def test_sharded_problem_allreduce_hook_world1():
         assert np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("method,family", [("pcg", "srht"), ("pcg", "sjlt"), ("ihs", "gaussian"),
+                                           ("ihs", "sjlt"), ("pcg", "srht-block")])
+def test_native_driver_matches_python_driver(method, family):
+    """adask_adaptive_run (C++) and the Python loop run the same kernels in the
+    same order: identical traces, bitwise."""
+    import paper_2104_14101_b200 as ak
+
+    j = np.arange(1, 97, dtype=float)
+    A, b, lam = _instance(4096, 96, j**-0.5, 1e-2, True)
+    p = ak.RegularizedProblem(A, b, 1e-2, lam)
+    sol = ak.direct_solve(p)
+    cfg = ak.AdaptiveConfig.for_method(method, 0.125, 4, 7, family, 3)
+    x1, t1 = ak.adaptive_run(p, np.zeros(96), cfg, method=method, sol=sol, native=True, block=1024)
+    x2, t2 = ak.adaptive_run(p, np.zeros(96), cfg, method=method, sol=sol, native=False, block=1024)
+    key = lambda tr: [(r.t, r.m, r.k, r.event, r.delta_tilde, r.delta_exact) for r in tr.records]  # noqa: E731
+    assert key(t1) == key(t2)
+    assert np.array_equal(x1, x2)
