@@ -28,382 +28,18 @@ namespace cg = cooperative_groups;
 
 namespace adask {
 
+// The kernel body is generic in the tile edge NB; NB = 64 and NB = 32 are
+// both compiled (namespaces chol64 / chol32).  NB = 32 halves the length of the
+// latency-bound diagonal factorization that sits on the critical path of
+// every panel, at the price of twice as many panels.
+namespace chol64 {
 constexpr int NB = 64;
-constexpr int NBP = NB + 1;  // padded SMEM row pitch (doubles)
-constexpr int kCholThreads = 256;
-
-struct CholArgs {
-  void* M;    // kp x kp, lower = input; reused as scratch
-  void* L;    // kp x kp output (upper pre-zeroed)
-  void* Li;   // kp x kp output L^-1 (upper pre-zeroed)
-  void* LiT;  // kp x kp output L^-T (lower pre-zeroed)
-  int kp, nblk, k;
-  int* info;
-  unsigned long long* tlog;  // optional phase timestamps (ADASK_CHOL_TRACE)
-};
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TMARK(idx)                                                   \
-  do {                                                               \
-    if (a.tlog && blockIdx.x == 0 && threadIdx.x == 0) a.tlog[idx] = gtimer(); \
-  } while (0)
-
-// 64 x 64 tile <-> SMEM (fp64), 16-byte vector accesses, all loads in flight.
-template <typename T>
-__device__ __forceinline__ void tile_load(double (*s)[NBP], const T* base, int ld, int bi, int bj) {
-  const T* p = base + (int64_t)bi * NB * ld + (int64_t)bj * NB;
-  constexpr int V = 16 / sizeof(T);            // elements per vector
-  constexpr int PER = NB * NB / V / kCholThreads;  // vectors per thread
-  using VT = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-  VT v[PER];
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int idx = threadIdx.x + kCholThreads * q;
-    const int r = idx / (NB / V), c = (idx % (NB / V)) * V;
-    v[q] = *reinterpret_cast<const VT*>(p + (int64_t)r * ld + c);
-  }
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int idx = threadIdx.x + kCholThreads * q;
-    const int r = idx / (NB / V), c = (idx % (NB / V)) * V;
-    const T* e = reinterpret_cast<const T*>(&v[q]);
-#pragma unroll
-    for (int u = 0; u < V; ++u) s[r][c + u] = (double)e[u];
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void tile_store(T* base, int ld, int bi, int bj, const double (*s)[NBP],
-                                           bool transpose = false, int lower_only = 0) {
-  T* p = base + (int64_t)bi * NB * ld + (int64_t)bj * NB;
-  constexpr int V = 16 / sizeof(T);
-  constexpr int PER = NB * NB / V / kCholThreads;
-  using VT = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int idx = threadIdx.x + kCholThreads * q;
-    const int r = idx / (NB / V), c = (idx % (NB / V)) * V;
-    VT v;
-    T* e = reinterpret_cast<T*>(&v);
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      double x = transpose ? s[c + u][r] : s[r][c + u];
-      if (lower_only == 1 && c + u > r) x = 0.0;  // lower triangle of the tile
-      if (lower_only == 2 && c + u < r) x = 0.0;  // upper triangle of the tile
-      e[u] = (T)x;
-    }
-    *reinterpret_cast<VT*>(p + (int64_t)r * ld + c) = v;
-  }
-}
-
-// acc[a][b] += sum_k A[r_a][k] * (TB ? B[c_b][k] : B[k][c_b]),
-// r_a = tr + 16a, c_b = tc + 16b.
-template <bool TB>
-__device__ __forceinline__ void tile_mma(const double (*A)[NBP], const double (*B)[NBP],
-                                         double acc[4][4]) {
-  const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
-#pragma unroll 8
-  for (int k = 0; k < NB; ++k) {
-    double a[4], b[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = A[tr + 16 * i][k];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = TB ? B[tc + 16 * j][k] : B[k][tc + 16 * j];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-  }
-}
-
-__device__ __forceinline__ void acc_to_tile(double (*C)[NBP], const double acc[4][4], double scale) {
-  const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) C[tr + 16 * i][tc + 16 * j] = scale * acc[i][j];
-}
-
-__device__ __forceinline__ void acc_zero(double acc[4][4]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-}
-
-__device__ __forceinline__ unsigned long long gtimer2() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Lower-triangle enumeration ordered by decreasing column: the trailing
-// triangle {j < l <= i < 64} of pivot step j is the prefix of length
-// (63 - j)(64 - j) / 2.  Entry = i | l << 8.
-__device__ void build_tri_table(unsigned short* tab) {
-  for (int e = threadIdx.x; e < NB * (NB - 1) / 2; e += blockDim.x) {
-    // invert the prefix sums: column l holds 64 - l entries
-    int l = NB - 1, base = 0;
-    while (e >= base + (NB - l)) {
-      base += NB - l;
-      --l;
-    }
-    const int i = l + (e - base);
-    tab[e] = (unsigned short)(i | (l << 8));
-  }
-}
-
-// Factor the 64 x 64 tile in S (lower triangle read) in place -- L, strict
-// upper zeroed -- and write X = L^-1.  Compact, rolled loops throughout: this
-// runs once per panel, so straight-line unrolled code would stream through a
-// cold instruction cache.  Factor: one pivot per step, the live trailing
-// triangle spread evenly over the CTA via the precomputed table.  Inverse:
-// warp w owns columns 8w..8w+7, lanes own rows lane and lane+32, finalized
-// rows broadcast by shuffles (no block barrier inside the loop).
-__device__ void diag_factor(double (*S)[NBP], double (*X)[NBP], const unsigned short* tab, int* info,
-                            int goff, int kvalid, unsigned long long* tl = nullptr) {
-  __shared__ double rinv[NB];
-  if (tl && threadIdx.x == 0) tl[0] = gtimer2();
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-#pragma unroll 1
-  for (int j = 0; j < NB; ++j) {
-    const double pj = S[j][j];
-    const double rd = rsqrt(pj);
-    if (t > j && t < NB) S[t][j] *= rd;
-    if (t == 0) {
-      if ((!(pj > 0.0) || !isfinite(pj)) && goff + j < kvalid) atomicCAS(info, 0, goff + j + 1);
-      rinv[j] = rd;
-    }
-    __syncthreads();
-    if (t == 0) S[j][j] = pj * rd;
-    const int T = (NB - 1 - j) * (NB - j) / 2;
-#pragma unroll 1
-    for (int e = t; e < T; e += kCholThreads) {
-      const int il = tab[e], i = il & 0xff, l = il >> 8;
-      S[i][l] = fma(-S[i][j], S[l][j], S[i][l]);
-    }
-    __syncthreads();
-  }
-  if (tl && threadIdx.x == 0) tl[1] = gtimer2();
-  for (int e = t; e < NB * NB; e += blockDim.x) {
-    const int i = e >> 6, j = e & 63;
-    if (j > i) S[i][j] = 0.0;
-  }
-  __syncthreads();
-  double acc[2][8];
-  const int c0 = warp * 8;
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[h][q] = (lane + 32 * h == c0 + q) ? 1.0 : 0.0;
-#pragma unroll 1
-  for (int i = 0; i < NB; ++i) {
-    const int owner = i & 31, hi = i >> 5;
-    const double ri = rinv[i];
-    double xi[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      double v = hi ? acc[1][q] : acc[0][q];
-      v = __shfl_sync(0xffffffffu, v, owner);
-      xi[q] = (c0 + q <= i) ? v * ri : 0.0;
-    }
-    if (lane == owner) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (hi) acc[1][q] = xi[q];
-        else acc[0][q] = xi[q];
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = lane + 32 * h;
-      const double lri = r > i ? S[r][i] : 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[h][q] = fma(-lri, xi[q], acc[h][q]);
-    }
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) X[lane + 32 * h][c0 + q] = acc[h][q];
-  __syncthreads();
-  if (tl && threadIdx.x == 0) tl[2] = gtimer2();
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ double csm[];
-  double(*sA)[NBP] = reinterpret_cast<double(*)[NBP]>(csm);
-  double(*sB)[NBP] = reinterpret_cast<double(*)[NBP]>(csm + NB * NBP);
-  double(*sC)[NBP] = reinterpret_cast<double(*)[NBP]>(csm + 2 * NB * NBP);
-  T* M = reinterpret_cast<T*>(a.M);
-  T* L = reinterpret_cast<T*>(a.L);
-  T* Li = reinterpret_cast<T*>(a.Li);
-  T* LiT = reinterpret_cast<T*>(a.LiT);
-  const int ld = a.kp, nblk = a.nblk;
-  const int G = gridDim.x, b = blockIdx.x;
-  double acc[4][4];
-  __shared__ unsigned short tri_tab[NB * (NB - 1) / 2];
-  build_tri_table(tri_tab);
-  __syncthreads();
-  TMARK(0);
-
-  // prologue: diagonal block 0
-  if (b == 0) {
-    tile_load<T>(sA, M, ld, 0, 0);
-    __syncthreads();
-    TMARK(3 * nblk + 4);
-    diag_factor(sA, sB, tri_tab, a.info, 0, a.k, a.tlog ? a.tlog + 3 * nblk + 8 : nullptr);
-    TMARK(3 * nblk + 5);
-    tile_store<T>(L, ld, 0, 0, sA, false, 1);
-    tile_store<T>(Li, ld, 0, 0, sB, false, 1);
-    __syncthreads();
-    TMARK(3 * nblk + 6);
-  }
-  grid.sync();
-  TMARK(1);
-  for (int j = 0; j + 1 < nblk; ++j) {
-    // ---- trsm: L_ij = A_ij Dinv_j^T, i > j
-    bool have = false;
-    for (int i = j + 1 + b; i < nblk; i += G) {
-      if (!have) {
-        tile_load<T>(sB, Li, ld, j, j);
-        have = true;
-      }
-      tile_load<T>(sA, M, ld, i, j);
-      __syncthreads();
-      acc_zero(acc);
-      tile_mma<true>(sA, sB, acc);
-      acc_to_tile(sC, acc, 1.0);
-      __syncthreads();
-      tile_store<T>(L, ld, i, j, sC);
-      __syncthreads();
-    }
-    grid.sync();
-    TMARK(2 + 3 * j);
-    // ---- syrk: A_il -= L_ij L_lj^T for j < l <= i.  CTA 0 owns the next
-    // diagonal tile and factors it right away (lookahead); the other CTAs
-    // share the remaining tiles.
-    const int Tn = nblk - j - 1;
-    const int ntiles = Tn * (Tn + 1) / 2;
-    const int t_first = (G == 1 || b == 0) ? 0 : b;
-    const int t_step = G == 1 ? 1 : (b == 0 ? ntiles : G - 1);
-    for (int t = t_first; t < ntiles; t += t_step) {
-      int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-      while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
-      while (ii * (ii + 1) / 2 > t) --ii;
-      const int ll = t - ii * (ii + 1) / 2;
-      const int i = j + 1 + ii, l = j + 1 + ll;
-      tile_load<T>(sA, L, ld, i, j);
-      tile_load<T>(sB, L, ld, l, j);
-      tile_load<T>(sC, M, ld, i, l);
-      __syncthreads();
-      acc_zero(acc);
-      tile_mma<true>(sA, sB, acc);
-      {
-        const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) sC[tr + 16 * x][tc + 16 * y] -= acc[x][y];
-      }
-      __syncthreads();
-      if (t == 0) {
-        // the updated diagonal tile j+1 is final: factor it now
-        diag_factor(sC, sB, tri_tab, a.info, (j + 1) * NB, a.k);
-        tile_store<T>(L, ld, j + 1, j + 1, sC, false, 1);
-        tile_store<T>(Li, ld, j + 1, j + 1, sB, false, 1);
-      } else {
-        tile_store<T>(M, ld, i, l, sC);
-      }
-      __syncthreads();
-    }
-    grid.sync();
-    TMARK(3 + 3 * j);
-  }
-  TMARK(3 * nblk + 1);
-
-  // ---- inverse by recursive doubling: I21 = -I22 (L21 I11), scratch in M
-  for (int s = 1; s < nblk; s <<= 1) {
-    // step a: Tmp(i, l) = sum_{p=l}^{b0+s-1} L(i, p) Li(p, l),  i in 2-range, l in 1-range
-    const int npairs = (nblk + 2 * s - 1) / (2 * s);
-    int work = 0;
-    for (int q = 0; q < npairs; ++q) {
-      const int b0 = q * 2 * s, r2 = min(s, nblk - (b0 + s));
-      if (r2 > 0) work += r2 * s;
-    }
-    for (int t = b; t < work; t += G) {
-      int q = 0, tt = t, b0 = 0, r2 = 0;
-      for (;; ++q) {
-        b0 = q * 2 * s;
-        r2 = min(s, nblk - (b0 + s));
-        const int w = r2 > 0 ? r2 * s : 0;
-        if (tt < w) break;
-        tt -= w;
-      }
-      const int i = b0 + s + tt / s, l = b0 + tt % s;
-      acc_zero(acc);
-      for (int p = l; p < b0 + s; ++p) {
-        tile_load<T>(sA, L, ld, i, p);
-        tile_load<T>(sB, Li, ld, p, l);
-        __syncthreads();
-        tile_mma<false>(sA, sB, acc);
-        __syncthreads();
-      }
-      acc_to_tile(sC, acc, 1.0);
-      __syncthreads();
-      tile_store<T>(M, ld, i, l, sC);
-      __syncthreads();
-    }
-    grid.sync();
-    // step b: Li(i, l) = -sum_{p=b0+s}^{i} Li(i, p) Tmp(p, l)
-    for (int t = b; t < work; t += G) {
-      int q = 0, tt = t, b0 = 0, r2 = 0;
-      for (;; ++q) {
-        b0 = q * 2 * s;
-        r2 = min(s, nblk - (b0 + s));
-        const int w = r2 > 0 ? r2 * s : 0;
-        if (tt < w) break;
-        tt -= w;
-      }
-      const int i = b0 + s + tt / s, l = b0 + tt % s;
-      acc_zero(acc);
-      for (int p = b0 + s; p <= i; ++p) {
-        tile_load<T>(sA, Li, ld, i, p);
-        tile_load<T>(sB, M, ld, p, l);
-        __syncthreads();
-        tile_mma<false>(sA, sB, acc);
-        __syncthreads();
-      }
-      acc_to_tile(sC, acc, -1.0);
-      __syncthreads();
-      tile_store<T>(Li, ld, i, l, sC);
-      __syncthreads();
-    }
-    grid.sync();
-  }
-
-  TMARK(3 * nblk + 2);
-  // ---- L^-T: LiT(l, i) = Li(i, l)^T for l <= i
-  const int nt = nblk * (nblk + 1) / 2;
-  for (int t = b; t < nt; t += G) {
-    int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
-    while (ii * (ii + 1) / 2 > t) --ii;
-    const int ll = t - ii * (ii + 1) / 2;
-    tile_load<T>(sA, Li, ld, ii, ll);
-    __syncthreads();
-    tile_store<T>(LiT, ld, ll, ii, sA, true, ii == ll ? 2 : 0);
-    __syncthreads();
-  }
-  grid.sync();
-  TMARK(3 * nblk + 3);
-}
+#include "chol_impl.cuh"
+}  // namespace chol64
+namespace chol32 {
+constexpr int NB = 32;
+#include "chol_impl.cuh"
+}  // namespace chol32
 
 template <typename T>
 __global__ void k_pad_identity(T* M, int k, int kp) {
@@ -427,7 +63,10 @@ int pad_identity(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, cuda
 int chol_factor_inverse(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, void* L, void* Li,
                         void* LiT, int64_t* info_host, cudaStream_t st) {
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
-  if (kp % NB || kp < k) return fail(ADASK_E_ARG, "chol: bad padding");
+  // tile edge: 32 unless overridden (ADASK_CHOL_NB=64)
+  int nb = 32;
+  if (const char* e = getenv("ADASK_CHOL_NB")) nb = atoi(e) == 64 ? 64 : 32;
+  if (kp % nb || kp < k) return fail(ADASK_E_ARG, "chol: bad padding");
   void* wsp = nullptr;
   ADASK_TRY(ctx->ws[WS_CHOL].get(256, st, &wsp));
   int* info = (int*)wsp;
@@ -435,51 +74,34 @@ int chol_factor_inverse(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t k
   ADASK_CUDA(cudaMemsetAsync(L, 0, (size_t)kp * kp * esz, st));
   ADASK_CUDA(cudaMemsetAsync(Li, 0, (size_t)kp * kp * esz, st));
   ADASK_CUDA(cudaMemsetAsync(LiT, 0, (size_t)kp * kp * esz, st));
-  const int nblk_ = (int)(kp / NB);
+  const int nblk = (int)(kp / nb);
   unsigned long long* tlog = nullptr;
   const bool trace = getenv("ADASK_CHOL_TRACE") != nullptr;
   if (trace) {
-    ADASK_CUDA(cudaMallocAsync((void**)&tlog, (3 * nblk_ + 16) * sizeof(unsigned long long), st));
-    ADASK_CUDA(cudaMemsetAsync(tlog, 0, (3 * nblk_ + 16) * sizeof(unsigned long long), st));
+    ADASK_CUDA(cudaMallocAsync((void**)&tlog, (3 * nblk + 16) * sizeof(unsigned long long), st));
+    ADASK_CUDA(cudaMemsetAsync(tlog, 0, (3 * nblk + 16) * sizeof(unsigned long long), st));
   }
-  CholArgs a{M, L, Li, LiT, (int)kp, nblk_, (int)k, info, tlog};
-  const int smem = 3 * NB * NBP * (int)sizeof(double);
-  void* fn = dtype == ADASK_F64 ? (void*)k_chol_coop<double> : (void*)k_chol_coop<float>;
-  ADASK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  int per_sm = 0;
-  ADASK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCholThreads, smem));
-  int nsm = kNumSMs;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
-  if (per_sm < 1) return fail(ADASK_E_CUDA, "chol: kernel cannot be resident");
-  int grid = nsm;  // one CTA per SM
-  const int nblk = (int)(kp / NB);
-  const int maxwork = nblk * (nblk + 1) / 2;
-  if (grid > maxwork) grid = std::max(1, maxwork);
-  if (const char* g = getenv("ADASK_CHOL_GRID")) grid = std::max(1, atoi(g));
-  void* args[] = {&a};
-  ADASK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kCholThreads), args, smem, st));
-  ADASK_LAUNCHED(ctx);
+  int grid = 0;
+  if (nb == 64)
+    ADASK_TRY(chol64::launch(ctx, dtype, M, k, kp, L, Li, LiT, info, tlog, st, &grid));
+  else
+    ADASK_TRY(chol32::launch(ctx, dtype, M, k, kp, L, Li, LiT, info, tlog, st, &grid));
   ADASK_CUDA(cudaMemcpyAsync(ctx->pinned_flags, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   ADASK_CUDA(cudaStreamSynchronize(st));
   if (trace) {
-    std::vector<unsigned long long> tl(3 * nblk_ + 16);
+    std::vector<unsigned long long> tl(3 * nblk + 16);
     cudaMemcpy(tl.data(), tlog, tl.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(tlog);
     double diag = (tl[1] - tl[0]) * 1e-3, trsm = 0, syrk = 0;
-    for (int j = 0; j + 1 < nblk_; ++j) {
+    for (int j = 0; j + 1 < nblk; ++j) {
       const unsigned long long t0 = j == 0 ? tl[1] : tl[3 * j];
       trsm += (tl[2 + 3 * j] - t0) * 1e-3;
       syrk += (tl[3 + 3 * j] - tl[2 + 3 * j]) * 1e-3;
     }
-    fprintf(stderr, "[chol k=%lld kp=%lld grid=%d] diag %.1f us, trsm %.1f us, syrk %.1f us, inverse %.1f us, "
-            "transpose %.1f us, total %.1f us\n", (long long)k, (long long)kp, grid, diag, trsm, syrk,
-            (tl[3 * nblk_ + 2] - tl[3 * nblk_ + 1]) * 1e-3, (tl[3 * nblk_ + 3] - tl[3 * nblk_ + 2]) * 1e-3,
-            (tl[3 * nblk_ + 3] - tl[0]) * 1e-3);
-    fprintf(stderr, "   prologue: load %.1f us, factor %.1f us, store %.1f us\n", (tl[3 * nblk_ + 4] - tl[0]) * 1e-3,
-            (tl[3 * nblk_ + 5] - tl[3 * nblk_ + 4]) * 1e-3, (tl[3 * nblk_ + 6] - tl[3 * nblk_ + 5]) * 1e-3);
-    fprintf(stderr, "   diag: factor loop %.2f us, inverse %.2f us\n", (tl[3 * nblk_ + 9] - tl[3 * nblk_ + 8]) * 1e-3,
-            (tl[3 * nblk_ + 10] - tl[3 * nblk_ + 9]) * 1e-3);
-
+    fprintf(stderr, "[chol NB=%d k=%lld kp=%lld grid=%d] diag %.1f us, trsm %.1f us, syrk %.1f us, inverse %.1f us, "
+            "transpose %.1f us, total %.1f us\n", nb, (long long)k, (long long)kp, grid, diag, trsm, syrk,
+            (tl[3 * nblk + 2] - tl[3 * nblk + 1]) * 1e-3, (tl[3 * nblk + 3] - tl[3 * nblk + 2]) * 1e-3,
+            (tl[3 * nblk + 3] - tl[0]) * 1e-3);
   }
   const int h = ctx->pinned_flags[0];
   if (info_host) *info_host = h;
@@ -498,7 +120,7 @@ extern "C" int adask_cholesky(adask_ctx* ctx, int dtype, const void* M, int64_t 
   if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
   cudaStream_t st = S(stream);
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
-  const int64_t kp = cdiv(k, NB) * NB;
+  const int64_t kp = cdiv(k, 64) * 64;
   const size_t mat = (size_t)kp * kp * esz;
   char* work = nullptr;
   ADASK_CUDA(cudaMallocAsync((void**)&work, 4 * mat, st));
