@@ -156,30 +156,28 @@ def philox4x32_10(ctr: np.ndarray, key: tuple[int, int]) -> np.ndarray:
 
 def philox_gaussian(m: int, n: int, seed: int, col0: int = 0) -> np.ndarray:
     """Gaussian sketch matrix S (m x n), columns [col0, col0+n) of the global
-    matrix: S[k, i] = z / sqrt(m), z from Box-Muller on Philox4x32-10 with
-    counter (pair q = i >> 1 (lo, hi), row k, 0) and key = 64-bit seed; the even
-    column takes sqrt(-2 ln u1) cos(2 pi u2), the odd one the sin.  The
-    product's definition (rng.cuh: gaussian_pair_f64), restated."""
+    matrix (the product's definition, rng.cuh: gaussian_quad_f64, restated).
+    For global column i and row group g = k >> 2, Philox4x32-10 with counter
+    (i_lo, i_hi, g, 0) and key = 64-bit seed gives words o0..o3;
+    u_j = (o_j >> 9) 2^-23; (z0, z1) = sqrt(-2 ln(1 - u0)) (cos, sin)(2 pi u1),
+    (z2, z3) likewise from (u2, u3); S[k, i] = z_{k & 3} / sqrt(m)."""
     key = (int(seed) & 0xFFFFFFFF, (int(seed) >> 32) & 0xFFFFFFFF)
-    q0, q1 = col0 >> 1, (col0 + n + 1) >> 1
-    q = np.arange(q0, q1, dtype=np.uint64)
-    k = np.arange(m, dtype=np.uint64)
-    ctr = np.zeros((m, q.size, 4), dtype=np.uint64)
-    ctr[..., 0] = (q & np.uint64(0xFFFFFFFF))[None, :]
-    ctr[..., 1] = (q >> np.uint64(32))[None, :]
-    ctr[..., 2] = k[:, None]
-    r = philox4x32_10(ctr, key).astype(np.uint64)
-    a = (r[..., 1] << np.uint64(32)) | r[..., 0]
-    b = (r[..., 3] << np.uint64(32)) | r[..., 2]
-    ua = (a >> np.uint64(11)).astype(np.float64) * 2.0**-53
-    ub = (b >> np.uint64(11)).astype(np.float64) * 2.0**-53
-    rad = np.sqrt(-2.0 * np.log(1.0 - ua))
-    th = 6.283185307179586 * ub
-    Z = np.empty((m, 2 * q.size))
-    Z[:, 0::2] = rad * np.cos(th)
-    Z[:, 1::2] = rad * np.sin(th)
-    off = col0 - 2 * q0
-    return Z[:, off:off + n] / np.sqrt(m)
+    ngrp = (m + 3) // 4
+    i = np.arange(col0, col0 + n, dtype=np.uint64)
+    g = np.arange(ngrp, dtype=np.uint64)
+    ctr = np.zeros((ngrp, n, 4), dtype=np.uint64)
+    ctr[..., 0] = (i & np.uint64(0xFFFFFFFF))[None, :]
+    ctr[..., 1] = (i >> np.uint64(32))[None, :]
+    ctr[..., 2] = g[:, None]
+    o = philox4x32_10(ctr, key)
+    u = (o >> np.uint32(9)).astype(np.float64) * 2.0**-23
+    Z = np.empty((ngrp, 4, n))
+    for p in range(2):
+        rad = np.sqrt(-2.0 * np.log(1.0 - u[..., 2 * p]))
+        th = 6.283185307179586 * u[..., 2 * p + 1]
+        Z[:, 2 * p] = rad * np.cos(th)
+        Z[:, 2 * p + 1] = rad * np.sin(th)
+    return Z.reshape(4 * ngrp, n)[:m] / np.sqrt(m)
 
 
 def sketch_gaussian(A: np.ndarray, m: int, seed: int, S: np.ndarray | None = None) -> np.ndarray:

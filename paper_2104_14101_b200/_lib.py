@@ -13,7 +13,7 @@ from pathlib import Path
 
 from . import errors
 
-LIB_PATH = Path(__file__).resolve().parent / "libadask.so"
+LIB_PATH = Path(os.environ.get("ADASK_LIB") or Path(__file__).resolve().parent / "libadask.so")
 
 ADASK_OK = 0
 E_DIM, E_NOT_SPD, E_NOT_POW2, E_SKETCH_TOO_LARGE, E_SPARSITY = 1, 2, 3, 4, 5

@@ -57,7 +57,8 @@ def compile_one(src: Path, verbose: bool, force: bool) -> Path:
     obj = BUILD / (src.stem + ".o")
     if not force and not _needs(obj, src):
         return obj
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    extra = os.environ.get("ADASK_NVCC_EXTRA", "").split()  # development builds only
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -33,7 +33,8 @@ extern "C" int adask_sketch_gaussian(adask_ctx* ctx, int dtype, const void* A, i
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
   const bool accumulate = (flags & ADASK_ACCUMULATE) != 0;
   ProfScope prof(ctx, PK_GAUSS, st, (double)n_local * d * esz, 2.0 * (double)m * n_local * d);
-  if ((flags & ADASK_TF32) && dtype == ADASK_F32) {
+  // tcgen05 path needs 16-byte aligned rows (TMA); otherwise the FP32-pipe GEMM
+  if ((flags & ADASK_TF32) && dtype == ADASK_F32 && lda % 4 == 0 && ((uintptr_t)A & 15) == 0) {
     return gauss_tc_impl(ctx, (const float*)A, n_local, d, lda, row0, m, key, (float*)SA, ldsa,
                          accumulate, st);
   }

@@ -182,19 +182,18 @@ int pcg_integers_impl(adask_ctx* ctx, const adask_pcg64* g, uint64_t first, int6
 // ---------------------------------------------------------------- Philox normals
 template <typename T>
 __global__ void k_philox_gaussian(int64_t m, int64_t col0, int64_t ncols, uint32_t k0, uint32_t k1,
-                                  double inv_scale_div, T* __restrict__ out, int64_t ldo) {
-  // one thread per (row k, column pair); grid.y tiles rows
-  int64_t k = blockIdx.y;
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // local pair slot
-  int64_t gfirst = col0 & ~1ll;                                // first global even column
-  int64_t i_even = gfirst + 2 * p;
-  if (i_even >= col0 + ncols) return;
-  double z0, z1;
-  gaussian_pair_f64((uint64_t)i_even >> 1, (uint32_t)k, k0, k1, z0, z1);
-  T* row = out + k * ldo;
-  if (i_even >= col0) row[i_even - col0] = (T)(z0 / inv_scale_div);
-  if (i_even + 1 < col0 + ncols) row[i_even + 1 - col0] = (T)(z1 / inv_scale_div);
-  (void)m;
+                                  double sc, T* __restrict__ out, int64_t ldo) {
+  // one thread per (column, group of four sketch rows); grid.y tiles groups
+  const int64_t g = blockIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  double z[4];
+  gaussian_quad_f64((uint64_t)(col0 + c), (uint32_t)g, k0, k1, z);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t k = 4 * g + q;
+    if (k < m) out[k * ldo + c] = (T)(z[q] / sc);
+  }
 }
 
 }  // namespace adask
@@ -215,9 +214,8 @@ extern "C" int adask_philox_gaussian(adask_ctx* ctx, int dtype, int64_t m, int64
   if (m <= 0 || ncols < 0 || col0 < 0 || ldo < ncols || !out)
     return fail(ADASK_E_ARG, "philox_gaussian: bad arguments");
   if (ncols == 0) return ADASK_OK;
-  if (m > 65535) return fail(ADASK_E_ARG, "philox_gaussian: m > 65535 per call");
-  int64_t pairs = ((col0 + ncols + 1) >> 1) - (col0 >> 1);
-  dim3 grid((unsigned)cdiv(pairs, 256), (unsigned)m);
+  if (m > 4 * 65535) return fail(ADASK_E_ARG, "philox_gaussian: m > 262140 per call");
+  dim3 grid((unsigned)cdiv(ncols, 256), (unsigned)cdiv(m, 4));
   double sc = sqrt((double)m);
   uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
   if (dtype == ADASK_F64)
@@ -237,11 +235,11 @@ extern "C" int adask_philox_gaussian_host(int64_t m, int64_t col0, int64_t ncols
   if (m <= 0 || ncols < 0 || col0 < 0 || ldo < ncols || (ncols > 0 && !out))
     return fail(ADASK_E_ARG, "philox_gaussian_host: bad arguments");
   const double sc = sqrt((double)m);
-  for (int64_t k = 0; k < m; ++k)
+  for (int64_t g = 0; 4 * g < m; ++g)
     for (int64_t i = col0; i < col0 + ncols; ++i) {
-      double z0, z1;
-      gaussian_pair_f64((uint64_t)i >> 1, (uint32_t)k, (uint32_t)key, (uint32_t)(key >> 32), z0, z1);
-      out[k * ldo + (i - col0)] = ((i & 1) ? z1 : z0) / sc;
+      double z[4];
+      gaussian_quad_f64((uint64_t)i, (uint32_t)g, (uint32_t)key, (uint32_t)(key >> 32), z);
+      for (int q = 0; q < 4 && 4 * g + q < m; ++q) out[(4 * g + q) * ldo + (i - col0)] = z[q] / sc;
     }
   return ADASK_OK;
 }

@@ -66,31 +66,36 @@ struct U32Stream {
   }
 };
 
-// Gaussian sketch entry pair for global column pair q = i >> 1 and sketch row
-// k: Philox4x32-10(counter = (q_lo, q_hi, k, 0), key = (k0, k1)) -> two 53-bit
-// uniforms u = (hi:lo >> 11) * 2^-53; Box-Muller with u1 = 1 - u_a in (0, 1]:
-// z0 = sqrt(-2 ln u1) cos(2 pi u_b) (even column), z1 = ... sin(...) (odd).
-__host__ __device__ inline void gaussian_pair_f64(uint64_t q, uint32_t k, uint32_t k0, uint32_t k1,
-                                                  double& z0, double& z1) {
-  philox4 c{(uint32_t)q, (uint32_t)(q >> 32), k, 0u};
+// Gaussian sketch entries (the product's definition; oracle/philox_gaussian
+// restates it).  For global A row i and sketch-row group g = k >> 2:
+//   (o0, o1, o2, o3) = Philox4x32-10(counter = (i_lo, i_hi, g, 0), key = seed)
+//   u_j = (o_j >> 9) * 2^-23                      (23-bit uniforms in [0, 1))
+//   z0, z1 = sqrt(-2 ln(1 - u0)) * (cos, sin)(2 pi u1)
+//   z2, z3 = sqrt(-2 ln(1 - u2)) * (cos, sin)(2 pi u3)
+//   S[k, i] = z_{k & 3} / sqrt(m)
+// One Philox call feeds four consecutive sketch rows of one column, so the
+// tensor-core kernel (gauss_tc.cu) writes one 16-byte chunk per call.
+__host__ __device__ inline void gaussian_quad_f64(uint64_t i, uint32_t g, uint32_t k0, uint32_t k1,
+                                                  double z[4]) {
+  philox4 c{(uint32_t)i, (uint32_t)(i >> 32), g, 0u};
   philox4 r = philox4x32_10(c, k0, k1);
-  uint64_t a = ((uint64_t)r.y << 32) | r.x;
-  uint64_t b = ((uint64_t)r.w << 32) | r.z;
-  const double two_m53 = 1.1102230246251565e-16;  // 2^-53
-  double ua = (double)(a >> 11) * two_m53;
-  double ub = (double)(b >> 11) * two_m53;
-  double u1 = 1.0 - ua;
-  double rad = sqrt(-2.0 * log(u1));
-  double th = 6.283185307179586 * ub;
-  double s, co;
+  const double two_m23 = 1.1920928955078125e-07;  // 2^-23
+  const uint32_t o[4] = {r.x, r.y, r.z, r.w};
+  for (int p = 0; p < 2; ++p) {
+    double ua = (double)(o[2 * p] >> 9) * two_m23;
+    double ub = (double)(o[2 * p + 1] >> 9) * two_m23;
+    double rad = sqrt(-2.0 * log(1.0 - ua));
+    double th = 6.283185307179586 * ub;
+    double s, co;
 #if defined(__CUDA_ARCH__)
-  sincos(th, &s, &co);
+    sincos(th, &s, &co);
 #else
-  s = sin(th);
-  co = cos(th);
+    s = sin(th);
+    co = cos(th);
 #endif
-  z0 = rad * co;
-  z1 = rad * s;
+    z[2 * p] = rad * co;
+    z[2 * p + 1] = rad * s;
+  }
 }
 
 // Items [item0, item0 + count) of Generator.integers(0, m, size=total_items)

@@ -177,3 +177,51 @@ def test_cholesky_sizes(ak, k):
     Lo = np.linalg.cholesky(M)
     assert np.linalg.norm(L - Lo) <= 1e-11 * np.linalg.norm(Lo)
     assert np.allclose(np.triu(L, 1), 0.0)
+
+
+# ---------------------------------------------------------------- TF32 tcgen05 Gaussian sketch
+def _tf32_case(n, d, m, row0, seed, accumulate=False):
+    from paper_2104_14101_b200.embeddings import gaussian_dev
+
+    rng = np.random.default_rng(n + d + m)
+    A = rng.standard_normal((n, d)).astype(np.float32)
+    Ad = torch.from_numpy(A).cuda()
+    S = O.philox_gaussian(m, n, seed, col0=row0)
+    ref = S @ A.astype(np.float64)
+    bound = np.abs(S) @ np.abs(A.astype(np.float64))
+    base = None
+    if accumulate:
+        base = torch.from_numpy(rng.standard_normal((m, d)).astype(np.float32)).cuda()
+        out = base.clone()
+        got = gaussian_dev(Ad, m, seed, row0=row0, tf32=True, out=out, accumulate=True)
+        ref = ref + base.cpu().numpy()
+    else:
+        got = gaussian_dev(Ad, m, seed, row0=row0, tf32=True)
+    torch.cuda.synchronize()
+    got = got.cpu().numpy().astype(np.float64)
+    # tf32 operands (10-bit mantissa, both sides) + fp32 accumulation:
+    # |err| <= 2^-9 sum |S||A| elementwise, and ~1e-3 in Frobenius norm
+    err = np.abs(got - ref)
+    assert np.all(err <= 2.0**-9 * bound + 1e-5), float(np.max(err / (bound + 1e-30)))
+    assert np.linalg.norm(got - ref) <= 2e-3 * np.linalg.norm(ref)
+    return got
+
+
+@pytest.mark.parametrize("n,d,m,row0", [(3000, 300, 200, 7), (1000, 64, 128, 0), (777, 516, 4, 3), (777, 513, 5, 3),
+                                        (65536, 96, 64, 1 << 33), (20000, 1030, 300, 5),
+                                        (4096, 1024, 256, 0), (9000, 2048, 520, 77)])
+def test_gaussian_tf32_tcgen05_matches_oracle(n, d, m, row0):
+    _tf32_case(n, d, m, row0, seed=99 + n)
+
+
+def test_gaussian_tf32_accumulate_and_shards():
+    _tf32_case(5000, 200, 130, 11, seed=5, accumulate=True)
+    # two row shards with global row offsets sum to the whole sketch
+    from paper_2104_14101_b200.embeddings import gaussian_dev
+
+    rng = np.random.default_rng(1)
+    A = torch.from_numpy(rng.standard_normal((4096, 160)).astype(np.float32)).cuda()
+    whole = gaussian_dev(A, 96, 3, tf32=True)
+    part = gaussian_dev(A[:2048], 96, 3, tf32=True)
+    part = gaussian_dev(A[2048:], 96, 3, row0=2048, tf32=True, out=part, accumulate=True)
+    torch.testing.assert_close(part, whole, rtol=0, atol=2e-5)
