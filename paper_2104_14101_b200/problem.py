@@ -21,6 +21,15 @@ from .errors import DimensionMismatch
 __all__ = ["RegularizedProblem", "ExactSolution", "direct_solve", "exact_error"]
 
 
+def _all_finite(A: torch.Tensor) -> bool:
+    """isfinite over A in row chunks (no n x d temporary for the 32-64 GB configs)."""
+    rows = max(1, (1 << 26) // max(1, A.shape[1]))
+    ok = torch.ones((), dtype=torch.bool, device=A.device)
+    for r0 in range(0, A.shape[0], rows):
+        ok &= torch.isfinite(A[r0:r0 + rows]).all()
+    return bool(ok)
+
+
 class RegularizedProblem:
     """Data matrix A (n x d), targets B (d x c), scale nu, diagonal lam
     (problem.py:41-111).  Keyword-only extras: dtype (matrix precision),
@@ -51,7 +60,7 @@ class RegularizedProblem:
         if validate:
             if not bool(torch.isfinite(self.lam_dev).all()) or float(self.lam_dev.min()) < 1.0:
                 raise ValueError("lam entries must be finite and >= 1")
-            if not (bool(torch.isfinite(self.A).all()) and bool(torch.isfinite(self.Bt).all())):
+            if not (_all_finite(self.A) and bool(torch.isfinite(self.Bt).all())):
                 raise ValueError("A and B must be finite")
         self.row0 = int(row0)
         self.n_total = n if n_total is None else int(n_total)
