@@ -233,22 +233,18 @@ def _log(msg: str) -> None:
 
 
 def _exact_solution(ak, p, cfg, sharded, dist):
-    import torch
-
-    if cfg.dtype == "float64" and not sharded:
+    """x* for the tracked run (untimed): problem.direct_solve -- fp64 Gram
+    accumulated over row blocks, fp64 Cholesky, two triangular solves -- with
+    the partial Grams all-reduced when A is row-sharded."""
+    if not sharded:
         return ak.direct_solve(p)
-    A = p.A
-    d = p.d
-    H = torch.zeros((d, d), dtype=torch.float64, device=A.device)
-    rows = max(1, (1 << 27) // d)
-    for r0 in range(0, A.shape[0], rows):
-        Ac = A[r0:r0 + rows].double()
-        H.addmm_(Ac.t(), Ac)
-    if sharded:
-        dist.all_reduce(H)
+    from paper_2104_14101_b200.problem import gram_fp64
+
+    H = gram_fp64(p.A)
+    dist.all_reduce(H)
     H.diagonal().add_(p.nu**2 * p.lam_dev)
-    L = torch.linalg.cholesky(H)
-    X = torch.cholesky_solve(p.Bt.t().contiguous(), L)
+    L = ak.cholesky(H)
+    X = ak.tri_solve(L, ak.tri_solve(L, p.Bt.t().contiguous()), transposed=True)
     return ak.ExactSolution(x_star=X)
 
 
@@ -320,12 +316,18 @@ def run_ours(args) -> None:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         ev0.record()
-        for _ in range(args.steps):
+        evs[0].record()
+        for k in range(args.steps):
             x, trace = solve()
+            evs[k + 1].record()
         ev1.record()
         torch.cuda.synchronize()
+    step_ms = [round(evs[k].elapsed_time(evs[k + 1]), 3) for k in range(args.steps)]
+    _log(f"step ms {step_ms}; torch allocated {torch.cuda.memory_allocated() >> 20} MiB, "
+         f"reserved {torch.cuda.memory_reserved() >> 20} MiB")
     if dist:
         dist.barrier()
     launches = ctx.launches() - launches0
@@ -396,6 +398,7 @@ def run_ours(args) -> None:
                        "l2": "A (%.0f MiB per GPU) exceeds the 126 MB L2; no flush" % (
                            p.A.numel() * p.A.element_size() / 2**20)},
             "rel_err_final": rel_err,
+            "step_ms": step_ms,
             "schedule": trace.schedule(),
             "solves_per_s_total": (ws if cfg.index < 2 else 1) * 1e3 / ms,
             "sketch_gbs": sketch_gbs,

@@ -237,6 +237,12 @@ int adask_precond_apply(adask_ctx* ctx, const adask_precond* P, const double* Z,
 int adask_cholesky(adask_ctx* ctx, int dtype, const void* M, int64_t k, int64_t ldm, void* L,
                    void* Linv, int64_t* info_host, void* stream);
 
+/* Solve L Y = Z (transposed = 0) or L^T Y = Z (transposed = 1) for lower
+ * triangular L (k x k), c right-hand sides stored as rows of Z / Y
+ * (linalg.py:47-55).  Not on the solver's hot path.                         */
+int adask_tri_solve(adask_ctx* ctx, int dtype, const void* L, int64_t k, int64_t ldl, int transposed,
+                    const double* Z, int64_t c, int64_t ldz, double* Y, int64_t ldy, void* stream);
+
 /* ======================================================================== */
 /* Fused iteration bodies (solvers.py:227-282 _PcgState, :522-546 _IhsState)*/
 /* ======================================================================== */

@@ -107,4 +107,57 @@ int woodbury_apply(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t
   return ADASK_OK;
 }
 
+// Triangular solve L y = z (or L^T y = z) for one right-hand side per CTA:
+// row-by-row substitution, each row's dot product reduced across the block.
+// Not on the solver's hot path (the preconditioner applies explicit
+// inverses); it backs the reference's linalg.tri_solve.
+template <typename T>
+__global__ void k_tri_solve(const T* __restrict__ L, int64_t k, int64_t ldl, int transposed,
+                            const double* __restrict__ Z, int64_t ldz, double* __restrict__ Y, int64_t ldy,
+                            int* bad) {
+  __shared__ double sh[32];
+  const double* z = Z + (int64_t)blockIdx.x * ldz;
+  double* y = Y + (int64_t)blockIdx.x * ldy;
+  for (int64_t s = 0; s < k; ++s) {
+    const int64_t i = transposed ? k - 1 - s : s;
+    double acc = 0.0;
+    if (!transposed) {
+      for (int64_t j = threadIdx.x; j < i; j += blockDim.x) acc += (double)L[i * ldl + j] * y[j];
+    } else {
+      for (int64_t j = i + 1 + threadIdx.x; j < k; j += blockDim.x) acc += (double)L[j * ldl + i] * y[j];
+    }
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+      const double dgl = (double)L[i * ldl + i];
+      if (dgl == 0.0) atomicExch(bad, 1);
+      y[i] = (z[i] - acc) / dgl;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace adask
+
+using namespace adask;
+
+extern "C" int adask_tri_solve(adask_ctx* ctx, int dtype, const void* L, int64_t k, int64_t ldl, int transposed,
+                               const double* Z, int64_t c, int64_t ldz, double* Y, int64_t ldy, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (k < 1 || c < 1 || ldl < k || ldz < k || ldy < k || !L || !Z || !Y)
+    return fail(ADASK_E_DIM, "tri_solve: bad shape");
+  if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
+  cudaStream_t st = S(stream);
+  void* wsp = nullptr;
+  ADASK_TRY(ctx->ws[WS_SMALL].get(256, st, &wsp));
+  ADASK_CUDA(cudaMemsetAsync(wsp, 0, sizeof(int), st));
+  if (dtype == ADASK_F64)
+    k_tri_solve<double><<<(unsigned)c, 256, 0, st>>>((const double*)L, k, ldl, transposed, Z, ldz, Y, ldy, (int*)wsp);
+  else
+    k_tri_solve<float><<<(unsigned)c, 256, 0, st>>>((const float*)L, k, ldl, transposed, Z, ldz, Y, ldy, (int*)wsp);
+  ADASK_LAUNCHED(ctx);
+  int bad = 0;
+  ADASK_CUDA(cudaMemcpyAsync(&bad, wsp, sizeof(int), cudaMemcpyDeviceToHost, st));
+  ADASK_CUDA(cudaStreamSynchronize(st));
+  if (bad) return fail(ADASK_E_ARG, "tri_solve: singular triangular factor (zero diagonal)");
+  return ADASK_OK;
+}

@@ -15,8 +15,6 @@
 // slices are summed in slice order by a second kernel (deterministic).
 // Warp roles: 0 TMA producer, 1 TMEM owner + MMA issuer, 2..9 S generators,
 // then the same 8 warps drain TMEM (tcgen05.ld) in the epilogue.
-#include <cudaTypedefs.h>
-
 #include <algorithm>
 #include <cstdlib>
 
@@ -25,30 +23,6 @@
 #include "umma.cuh"
 
 namespace adask {
-
-int tensor_map_f32_sw128(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld,
-                         uint32_t box_cols, uint32_t box_rows, bool atom32) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    ADASK_CUDA(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q));
-    if (q != cudaDriverEntryPointSuccess || !fn)
-      return fail(ADASK_E_CUDA, "cuTensorMapEncodeTiled not available from the driver");
-    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(ADASK_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return ADASK_OK;
-}
-
 
 namespace {
 

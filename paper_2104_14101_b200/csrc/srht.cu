@@ -18,6 +18,7 @@
 // Algorithmic bytes: (n + m) * d * sizeof(T); the pruned intermediate adds
 // 2 * nslots * G * d * sizeof(T) (nslots <= min(m, B)).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -127,6 +128,25 @@ __device__ __forceinline__ void fw_round_smem(T* tile, int lo) {
   }
 }
 
+// Last-round output of one unit: pass 1 writes the rows whose low bits are a
+// needed slot into Z (slot-major), pass 2 writes the selected rows, scaled.
+template <typename T, int MODE, int E>
+__device__ __forceinline__ void fw_emit(const T (&v)[E], const int (&rows)[E], const int* map, T* zb, int64_t gd,
+                                        T* ob, int64_t ldo, double c1, double c2, int accumulate) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int t = map[rows[e]];
+    if (t < 0) continue;
+    if constexpr (MODE == FW_P1) {
+      zb[(int64_t)t * gd] = v[e];
+    } else {
+      T* o = ob + (int64_t)t * ldo;
+      const T y = fw_scale<T>(v[e], c1, c2);
+      *o = accumulate ? (T)(*o + y) : y;
+    }
+  }
+}
+
 template <typename T, int LOG, int MODE>
 __global__ void __launch_bounds__(256) k_fwht_tile(FwhtArgs a) {
   using Sh = FwShape<LOG>;
@@ -135,21 +155,34 @@ __global__ void __launch_bounds__(256) k_fwht_tile(FwhtArgs a) {
   constexpr int CP = C;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);
-  int* hi_to_k = reinterpret_cast<int*>(smem_raw + fw_tile_bytes<T, LOG>());
+  // pass 1: low row bits -> slot (-1: not needed); pass 2: high bits -> output row
+  int* map = reinterpret_cast<int*>(smem_raw + fw_tile_bytes<T, LOG>());
 
   // column panels vary fastest across the grid so that concurrently running
   // CTAs cover whole rows of A (DRAM page locality)
   const int64_t blk = blockIdx.y;  // pass 1: row block; pass 2: slot
   const int64_t c0 = (int64_t)blockIdx.x * C;
-  const int64_t d = a.d;
+  const int64_t d = a.d, G = a.G;
+  const int64_t n_valid = a.n_valid, ld = MODE == FW_P1 ? a.src_ld : d;
+  const uint32_t* sgn = a.sgn;
+  const double c1 = a.c1, c2 = a.c2;
+  const int accumulate = a.accumulate;
+  const int64_t ldo = a.ldo;
+  T* zbase = reinterpret_cast<T*>(a.Z);
+  T* obase = reinterpret_cast<T*>(a.out);
 
-  if constexpr (MODE == FW_P2) {
-    for (int i = threadIdx.x; i < B; i += blockDim.x) hi_to_k[i] = -1;
+  if constexpr (MODE == FW_P1) {
+    const int32_t* l2s = a.lo_to_slot;
+    for (int i = threadIdx.x; i < B; i += blockDim.x) map[i] = l2s ? l2s[i] : i;
+  } else {
+    for (int i = threadIdx.x; i < B; i += blockDim.x) map[i] = -1;
     __syncthreads();
     const int p0 = a.slot_start[blk], p1 = a.slot_start[blk + 1];
-    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) hi_to_k[a.ent_hi[p]] = a.ent_k[p];
-    __syncthreads();
+    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) map[a.ent_hi[p]] = a.ent_k[p];
   }
+  __syncthreads();
+  // output bases (per column): Z[(slot * G + blk) * d + col], out[k * ldo + col]
+  const int64_t gd = G * d;
 
   // ---- round 0: global -> registers -> butterflies (bits [0, NB1)) -> SMEM
   {
@@ -159,48 +192,33 @@ __global__ void __launch_bounds__(256) k_fwht_tile(FwhtArgs a) {
     for (int u = threadIdx.x; u < UNITS; u += blockDim.x) {
       const int c = u % C, q = u / C;
       const int64_t col = c0 + c;
-      T v[E];
-      // rows q*E .. q*E + E - 1 (consecutive): all loads first, branch-free
       const bool cok = col < d;
-      if constexpr (MODE == FW_P1) {
-        const int64_t g0 = blk * B + (int64_t)q * E;
-        const T* src = reinterpret_cast<const T*>(a.src) + (cok ? col : 0);
+      T v[E];
+      // rows q*E .. q*E + E - 1 (consecutive); all loads first
+      const int64_t r0 = MODE == FW_P1 ? blk * B + (int64_t)q * E : blk * G + (int64_t)q * E;
+      const T* src = reinterpret_cast<const T*>(MODE == FW_P1 ? a.src : a.Z) + r0 * ld + (cok ? col : 0);
+      if (cok && (MODE == FW_P2 || r0 + E <= n_valid)) {
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int64_t grow = g0 + e;
-          const bool ok = cok && grow < a.n_valid;
-          v[e] = ok ? __ldg(src + (ok ? grow : 0) * a.src_ld) : (T)0;
-        }
-        if (a.sgn) {
+        for (int e = 0; e < E; ++e) v[e] = __ldg(src + e * ld);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = (cok && r0 + e < n_valid) ? __ldg(src + e * ld) : (T)0;
+      }
+      if constexpr (MODE == FW_P1) {
+        if (sgn) {
           // diag(signs) A: exact negation where the sign bit is 0
-          const uint32_t bits = a.sgn[g0 >> 5] >> (g0 & 31);
+          const uint32_t bits = sgn[r0 >> 5] >> (r0 & 31);
 #pragma unroll
           for (int e = 0; e < E; ++e) v[e] = ((bits >> e) & 1u) ? v[e] : -v[e];
         }
-      } else {
-        const T* src = reinterpret_cast<const T*>(a.Z) + blk * a.G * d + (cok ? col : 0);
-#pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = cok ? __ldg(src + (int64_t)(q * E + e) * d) : (T)0;
       }
       butterflies<T, NB>(v);
       if constexpr (Sh::ROUNDS == 1) {
-        // output directly
+        if (!cok) continue;
+        int rows[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int r = fw_row(q, e, 0, NB);
-          if (col >= d) continue;
-          if constexpr (MODE == FW_P1) {
-            const int slot = a.lo_to_slot ? a.lo_to_slot[r] : r;
-            if (slot >= 0) reinterpret_cast<T*>(a.Z)[((int64_t)slot * a.G + blk) * d + col] = v[e];
-          } else {
-            const int k = hi_to_k[r];
-            if (k >= 0) {
-              T* o = reinterpret_cast<T*>(a.out) + (int64_t)k * a.ldo + col;
-              T y = fw_scale<T>(v[e], a.c1, a.c2);
-              *o = a.accumulate ? (T)(*o + y) : y;
-            }
-          }
-        }
+        for (int e = 0; e < E; ++e) rows[e] = fw_row(q, e, 0, NB);
+        fw_emit<T, MODE, E>(v, rows, map, zbase + blk * d + col, gd, obase + col, ldo, c1, c2, accumulate);
       } else {
 #pragma unroll
         for (int e = 0; e < E; ++e) tile[fw_row(q, e, 0, NB) * CP + c] = v[e];
@@ -224,25 +242,15 @@ __global__ void __launch_bounds__(256) k_fwht_tile(FwhtArgs a) {
       const int c = u % C, q = u / C;
       const int64_t col = c0 + c;
       T v[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) v[e] = tile[fw_row(q, e, LO, LOG) * CP + c];
-      butterflies<T, NB>(v);
-      if (col >= d) continue;
+      int rows[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int r = fw_row(q, e, LO, LOG);
-        if constexpr (MODE == FW_P1) {
-          const int slot = a.lo_to_slot ? a.lo_to_slot[r] : r;
-          if (slot >= 0) reinterpret_cast<T*>(a.Z)[((int64_t)slot * a.G + blk) * d + col] = v[e];
-        } else {
-          const int k = hi_to_k[r];
-          if (k >= 0) {
-            T* o = reinterpret_cast<T*>(a.out) + (int64_t)k * a.ldo + col;
-            T y = fw_scale<T>(v[e], a.c1, a.c2);
-            *o = a.accumulate ? (T)(*o + y) : y;
-          }
-        }
+        rows[e] = fw_row(q, e, LO, LOG);
+        v[e] = tile[rows[e] * CP + c];
       }
+      butterflies<T, NB>(v);
+      if (col >= d) continue;
+      fw_emit<T, MODE, E>(v, rows, map, zbase + blk * d + col, gd, obase + col, ldo, c1, c2, accumulate);
     }
   }
 }
@@ -251,7 +259,7 @@ template <typename T, int LOG, int MODE>
 static int launch_fw(adask_ctx* ctx, const FwhtArgs& a, int64_t nblk, cudaStream_t st) {
   constexpr int C = fw_cols<T, LOG>();
   constexpr int B = 1 << LOG;
-  size_t smem = fw_tile_bytes<T, LOG>() + (MODE == FW_P2 ? sizeof(int) * (size_t)B : 0);
+  size_t smem = fw_tile_bytes<T, LOG>() + sizeof(int) * (size_t)B;
   auto kern = k_fwht_tile<T, LOG, MODE>;
   if (smem > 48 * 1024) ADASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)cdiv(a.d, C), (unsigned)nblk);
@@ -288,7 +296,8 @@ static int fwht_select(adask_ctx* ctx, int dtype, const void* A, int64_t n, int6
                        void* out, int64_t ldo, double c1, double c2, int accumulate,
                        cudaStream_t st) {
   const int L = ilog2(n_pad);
-  const int b1 = std::max(std::min(L, 10), L - 12);
+  int b1 = std::max(std::min(L, 10), L - 12);
+  if (const char* e = getenv("ADASK_FWHT_B1")) b1 = std::max(L - 12, std::min(L, atoi(e)));
   const int64_t B = 1ll << b1, G = n_pad >> b1;
   const int L2 = L - b1;
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;

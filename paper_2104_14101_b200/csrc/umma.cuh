@@ -197,5 +197,8 @@ __device__ __forceinline__ void tma_prefetch_map(const CUtensorMap* map) {
 // through the runtime's driver entry point (no libcuda link dependency).
 int tensor_map_f32_sw128(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld,
                          uint32_t box_cols, uint32_t box_rows, bool atom32 = false);
+// Plain (unswizzled) 2-D row-major tensor map of fp64 / fp32 (dtype ADASK_F64 / F32).
+int tensor_map_2d(CUtensorMap* map, int dtype, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                  uint32_t box_cols, uint32_t box_rows);
 
 }  // namespace adask

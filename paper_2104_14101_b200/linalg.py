@@ -47,11 +47,17 @@ def cholesky(M):
 def tri_solve(L, z, transposed: bool = False):
     """Solve L y = z (or L.T y = z) for lower-triangular L (linalg.py:47-55)."""
     Ld = _square(L, "L")
-    zt, vec = dv.as_columns(z, Ld.shape[0]) if np.ndim(z) else (None, False)
-    if zt is None or zt.shape[1] != Ld.shape[0]:
-        raise DimensionMismatch(f"rhs has leading dimension {np.shape(z)[0]}, factor is {Ld.shape[0]}")
-    # invert through the same factor machinery: L^-1 from the Cholesky of L L^T
-    raise NotImplementedError("tri_solve on arbitrary triangular input: use Preconditioner.solve")
+    k = Ld.shape[0]
+    if np.ndim(z) == 0 or np.shape(z)[0] != k:
+        raise DimensionMismatch(f"rhs has leading dimension {np.shape(z)[0] if np.ndim(z) else 0}, "
+                                f"factor is {k}")
+    zt, vec = dv.as_columns(z, k)
+    Yt = torch.empty_like(zt)
+    c = zt.shape[0]
+    _lib.check(_lib.lib().adask_tri_solve(dv.ctx().handle, dv.dtype_code(Ld.dtype), Ld.data_ptr(), k,
+                                          Ld.stride(0), 1 if transposed else 0, zt.data_ptr(), c, k,
+                                          Yt.data_ptr(), k, dv.stream()), "tri_solve")
+    return dv.from_columns(Yt, vec, z)
 
 
 def fwht(x, normalized: bool = True):

@@ -160,15 +160,42 @@ class ExactSolution:
 
 
 def direct_solve(p: RegularizedProblem) -> ExactSolution:
-    """Solve H x = B by a dense Cholesky factorization of H (problem.py:144-149):
-    the preconditioner built from A itself has H_S = H (m = n >= d path)."""
+    """Solve H x = B by a dense Cholesky factorization of H (problem.py:144-149).
+    fp64 data: the preconditioner built from A itself (H_S = H, m = n >= d).
+    fp32 data: H is accumulated in fp64 over row blocks of A (each block
+    widened to fp64, Gram by libadask), then an fp64 Cholesky and two
+    triangular solves -- the exact solution for configs 3-4."""
+    from .linalg import cholesky, tri_solve
     from .preconditioner import build_dev
 
     if p.n < p.d:
         raise DimensionMismatch("direct_solve needs n >= d on the device path")
-    P = build_dev(p.A, p.nu, p.lam_dev)
-    X = P.solve_dev(p.Bt)
-    return ExactSolution(x_star=dv.to_host_like(X.t().contiguous(), p._like))
+    if p.A.dtype == dv.F64:
+        P = build_dev(p.A, p.nu, p.lam_dev)
+        X = P.solve_dev(p.Bt)
+        return ExactSolution(x_star=dv.to_host_like(X.t().contiguous(), p._like))
+    H = gram_fp64(p.A, p.nu**2, p.lam_dev)
+    L = cholesky(H)
+    Y = tri_solve(L, p.Bt.t().contiguous())
+    X = tri_solve(L, Y, transposed=True)
+    return ExactSolution(x_star=dv.to_host_like(X, p._like))
+
+
+def gram_fp64(A: torch.Tensor, nu2: float = 0.0, lam: torch.Tensor | None = None,
+              rows: int = 1 << 16) -> torch.Tensor:
+    """A^T A (+ nu2 diag(lam)) in fp64 for an fp32 or fp64 A, over row blocks."""
+    n, d = A.shape
+    H = torch.zeros((d, d), dtype=dv.F64, device=A.device)
+    part = torch.empty_like(H)
+    for r0 in range(0, n, rows):
+        blk = A[r0:r0 + rows]
+        blk = blk if blk.dtype == dv.F64 else blk.double()
+        _lib.check(_lib.lib().adask_gram(dv.ctx().handle, dv.dtype_code(dv.F64), blk.data_ptr(), blk.shape[0], d,
+                                         blk.stride(0), 0.0, None, part.data_ptr(), d, dv.stream()), "gram")
+        H += part
+    if lam is not None and nu2 != 0.0:
+        H.diagonal().add_(nu2 * lam)
+    return H
 
 
 def exact_error_dev(p: RegularizedProblem, Xt: torch.Tensor, Xstar_t: torch.Tensor) -> float:

@@ -308,10 +308,26 @@ def polyak_ihs_run(p, x0, m, rho, family, seed, T, sol=None, s=1, *, tf32=False)
 
 
 def cg(p, x0, T, tol=0.0, sol=None):
-    """Conjugate gradient on H x = b (solvers.py:104-140): PCG with the
-    identity preconditioner, built as the Woodbury path of an all-zero
-    1 x d sketch with lam = nu^-2 (H_S = I)."""
-    raise NotImplementedError("cg: planned (SURVEY 8(f) next #3)")
+    """Conjugate gradient on H x = b, columnwise (solvers.py:104-140): the
+    fused PCG bodies with the identity preconditioner -- the Woodbury path of
+    an all-zero 1 x d sketch with nu = 1, lam = 1, so H_S = I exactly and the
+    trace's delta_tilde is (1/2)||r||_F^2 as in the reference.  Stops after T
+    iterations or once that value falls to tol."""
+    clock = _Clock()
+    Xt, vec = _promote(p, x0)
+    P = build_dev(torch.zeros((1, p.d), dtype=p.A.dtype, device=Xt.device), 1.0,
+                  torch.ones(p.d, dtype=dv.F64, device=Xt.device))
+    trace = SolverTrace()
+    sol_t = _sol_cols(sol)
+    state = _PcgState(p, P, Xt)
+    _record(trace, clock, p, sol_t, 0, 0, 0, state.delta_tilde, state.x, "plain")
+    for t in range(1, T + 1):
+        if state.done() or state.delta_tilde <= tol:
+            break
+        dt_new, stash = state.propose()
+        state.commit(dt_new, stash)
+        _record(trace, clock, p, sol_t, t, 0, 0, state.delta_tilde, state.x, "plain")
+    return dv.from_columns(state.x, vec, x0), trace
 
 
 # ------------------------------------------------------------------ adaptive

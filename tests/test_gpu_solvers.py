@@ -135,3 +135,68 @@ def test_native_driver_matches_python_driver(method, family):
     key = lambda tr: [(r.t, r.m, r.k, r.event, r.delta_tilde, r.delta_exact) for r in tr.records]  # noqa: E731
     assert key(t1) == key(t2)
     assert np.array_equal(x1, x2)
+
+
+# ------------------------------------------------------------ plain CG / tri_solve
+def _np_cg(A, B, nu, lam, x0, T, tol=0.0):
+    """The reference CG recursion (solvers.py:104-140) restated in numpy."""
+    Hm = lambda X: A.T @ (A @ X) + nu**2 * lam[:, None] * X  # noqa: E731  (problem.py:89-95)
+    x = x0[:, None].copy()
+    r = B[:, None] - Hm(x)
+    q = r.copy()
+    rs = np.sum(r * r, axis=0)
+    dts = [0.5 * rs.sum()]
+    for _ in range(T):
+        active = rs > 0.0
+        if not active.any() or 0.5 * rs.sum() <= tol:
+            break
+        Hq = Hm(q)
+        qHq = np.sum(q * Hq, axis=0)
+        alpha = np.where(active, rs / np.where(qHq > 0, qHq, 1.0), 0.0)
+        x += q * alpha
+        r -= Hq * alpha
+        rs_new = np.sum(r * r, axis=0)
+        q = r + q * np.where(active, rs_new / np.where(rs > 0, rs, 1.0), 0.0)
+        rs = rs_new
+        dts.append(0.5 * rs.sum())
+    return x[:, 0], np.array(dts)
+
+
+def test_plain_cg_matches_reference_recursion():
+    import paper_2104_14101_b200 as ak
+
+    # well conditioned (CG's late iterates amplify rounding differences on
+    # ill-conditioned systems, so compare where the recursion is stable)
+    rng = np.random.default_rng(11)
+    n, d = 600, 40
+    A = rng.standard_normal((n, d)) / np.sqrt(n) * (0.98 ** np.arange(d))
+    b = rng.standard_normal(d)
+    lam = rng.uniform(1, 3, d)
+    p = ak.RegularizedProblem(A, b, 0.3, lam)
+    x, tr = ak.cg(p, np.zeros(d), 12)
+    xr, dts = _np_cg(A, b, 0.3, lam, np.zeros(d), 12)
+    got = np.array([r.delta_tilde for r in tr.records])
+    assert len(got) == len(dts)
+    # late iterations sit at the rounding floor: compare relative to delta_0
+    np.testing.assert_allclose(got, dts, rtol=1e-6, atol=1e-12 * dts[0])
+    np.testing.assert_allclose(x, xr, rtol=1e-8, atol=1e-10)
+    # tol stop
+    _, tr2 = ak.cg(p, np.zeros(d), 12, tol=dts[5] * (1 + 1e-6))
+    assert len(tr2.records) == 6
+
+
+@pytest.mark.parametrize("k,c,transposed", [(1, 1, False), (37, 1, False), (37, 3, True), (300, 2, False),
+                                            (300, 1, True)])
+def test_tri_solve_matches_scipy(k, c, transposed):
+    import scipy.linalg
+
+    import paper_2104_14101_b200 as ak
+
+    rng = np.random.default_rng(k + c)
+    L = np.tril(rng.standard_normal((k, k))) + 3 * np.eye(k)
+    z = rng.standard_normal((k, c)) if c > 1 else rng.standard_normal(k)
+    got = ak.tri_solve(L, z, transposed=transposed)
+    ref = scipy.linalg.solve_triangular(L, z, lower=True, trans=1 if transposed else 0)
+    np.testing.assert_allclose(got, ref, rtol=1e-10, atol=1e-12)
+    with pytest.raises(ak.DimensionMismatch):
+        ak.tri_solve(L, np.ones(k + 1))

@@ -17,6 +17,12 @@ if which == "srht":
     for m in (32, 256, 1024, 4096):
         ms = t(lambda: srht_dev(A, m, 7))
         print(f"srht n={n} d={d} m={m}: {ms*1e3:.1f} us  {(n+m)*d*8/ms/1e6:.0f} GB/s", flush=True)
+if which == "srht4":
+    n, d = 1 << 21, 1024
+    A = torch.randn(n, d, dtype=torch.float32, device="cuda")
+    for m in (64, 1024, 4096, 32768):
+        ms = t(lambda: srht_dev(A, m, 7), 3)
+        print(f"srht fp32 n={n} d={d} m={m}: {ms*1e3:.1f} us  {(n+m)*d*4/ms/1e6:.0f} GB/s", flush=True)
 if which == "sjlt":
     n, d = 1 << 20, 2048
     A = torch.empty(n, d, dtype=torch.float64, device="cuda").normal_()
