@@ -346,7 +346,10 @@ def run_ours(args) -> None:
 
     # ---- roofline of the dominant unit
     pk = _peaks()
-    dom = max(prof, key=lambda k: prof[k]["ms"])
+    # roofline kernel: the streaming / tensor unit with the most device time
+    # (the build unit -- Gram, Cholesky, inverse -- is latency bound and is
+    # reported in `units`)
+    dom = max(("hess_mult", "srht", "sjlt", "gaussian"), key=lambda k: prof[k]["ms"])
     u = prof[dom]
     per_launch_ms = u["ms"] / max(u["count"], 1)
     tensor = dom == "gaussian" and tf32

@@ -122,6 +122,7 @@ struct adask_ctx {
   int prof = 0;
   std::vector<adask_prof_rec> prof_recs[adask::PK_COUNT];
   std::vector<cudaEvent_t> event_pool;
+  void* blas = nullptr;  // cublasHandle_t, created on first Gram (gram.cu)
 };
 
 namespace adask {

@@ -361,22 +361,34 @@ static int hess_partial_tma(adask_ctx* ctx, const T* A, int64_t n, int64_t d, in
 
 // out[j] = sum_b part[b][j]  (+ nu2 lam[j] x[j] - B[j])   fixed order.
 // Block = 32 columns x 8 b-groups.
-__global__ void k_hess_finish(const double* __restrict__ part, int nparts, int64_t d,
-                              const double* __restrict__ x, double nu2,
-                              const double* __restrict__ lam, const double* __restrict__ B,
-                              double* __restrict__ out, int epilogue) {
-  __shared__ double sh[8][33];
+__global__ void __launch_bounds__(1024) k_hess_finish(const double* __restrict__ part, int nparts, int64_t d,
+                                                      const double* __restrict__ x, double nu2,
+                                                      const double* __restrict__ lam,
+                                                      const double* __restrict__ B, double* __restrict__ out,
+                                                      int epilogue) {
+  // 32 columns x 32 partial groups; each thread sums its parts with four
+  // independent accumulators (all loads in flight at once), then group 0
+  // combines the 32 group sums -- a fixed order, so the result is deterministic
+  __shared__ double sh[32][33];
   const int cx = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * 32 + cx;
-  double s = 0.0;
-  if (j < d)
-    for (int b = g; b < nparts; b += 8) s += part[(int64_t)b * d + j];
-  sh[g][cx] = s;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (j < d) {
+    int b = g;
+    for (; b + 96 < nparts; b += 128) {
+      s0 += part[(int64_t)b * d + j];
+      s1 += part[(int64_t)(b + 32) * d + j];
+      s2 += part[(int64_t)(b + 64) * d + j];
+      s3 += part[(int64_t)(b + 96) * d + j];
+    }
+    for (; b < nparts; b += 32) s0 += part[(int64_t)b * d + j];
+  }
+  sh[g][cx] = (s0 + s1) + (s2 + s3);
   __syncthreads();
   if (g == 0 && j < d) {
     double t = sh[0][cx];
 #pragma unroll
-    for (int q = 1; q < 8; ++q) t += sh[q][cx];
+    for (int q = 1; q < 32; ++q) t += sh[q][cx];
     if (epilogue) {
       t += nu2 * (lam[j] * x[j]);
       if (B) t -= B[j];
@@ -540,7 +552,7 @@ int hess_mult_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t 
     } else {
       return fail(ADASK_E_ARG, "bad dtype %d", dtype);
     }
-    k_hess_finish<<<(unsigned)cdiv(d, 32), 256, 0, st>>>(part, nparts, d, x, nu2, lam,
+    k_hess_finish<<<(unsigned)cdiv(d, 32), 1024, 0, st>>>(part, nparts, d, x, nu2, lam,
                                                          B ? B + j * ldb : nullptr,
                                                          out + j * ldo, partial ? 0 : 1);
     ADASK_LAUNCHED(ctx);

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "gemm.cuh"
 #include "pcg64.cuh"
 
 namespace adask {
@@ -371,6 +372,7 @@ int adask_ctx_destroy(adask_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (auto& w : ctx->ws) w.release();
+  adask::blas_release(ctx);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
   delete ctx;

@@ -8,6 +8,8 @@
 //        woodbury out = (y - SA^T L^-T L^-1 SA y / lam) / nu^2,  y = z / lam
 #include "blas2.cuh"
 #include "chol.cuh"
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gemm.cuh"
 #include "precond.cuh"
@@ -110,12 +112,16 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
     if (s) break;
     void* M = wsp;
     double* kinv = (double*)((char*)wsp + gram_bytes);
+    const bool native = getenv("ADASK_GRAM_NATIVE") != nullptr;  // hand-written GEMM (comparison)
     if (P->path == 0) {
       // H_S = SA^T SA + nu^2 diag(lam)   (preconditioner.py:70)
-      s = gemm_impl(ctx, dtype, d, d, m, 1.0, SA, ldsa, true, SA, ldsa, false, nullptr, 0.0, M, kp,
-                    P->nu2, P->lam, true, st);
+      s = native ? gemm_impl(ctx, dtype, d, d, m, 1.0, SA, ldsa, true, SA, ldsa, false, nullptr, 0.0, M, kp,
+                             P->nu2, P->lam, true, st)
+                 : gram_dense(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
+    } else if (!native) {
+      // W_S = (SA / lam) SA^T + nu^2 I   (preconditioner.py:72-73)
+      s = gram_woodbury(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
     } else {
-      // W_S = (SA * (1/lam)) SA^T + nu^2 I   (preconditioner.py:72-73)
       k_recip<<<(unsigned)cdiv(d, 256), 256, 0, st>>>(P->lam, d, kinv);
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) {
@@ -182,8 +188,7 @@ extern "C" int adask_gram(adask_ctx* ctx, int dtype, const void* A, int64_t n, i
   ADASK_TRY(use_device(ctx));
   if (n < 0 || d < 1 || lda < d || ldo < d) return fail(ADASK_E_DIM, "gram: bad shape");
   cudaStream_t st = S(stream);
-  ADASK_TRY(gemm_impl(ctx, dtype, d, d, n, 1.0, A, lda, true, A, lda, false, nullptr, 0.0, out, ldo,
-                      lam ? nu2 : 0.0, lam, true, st));
+  ADASK_TRY(gram_dense(ctx, dtype, A, n, d, lda, lam ? nu2 : 0.0, lam, out, ldo, st));
   if (dtype == ADASK_F64)
     k_mirror_lower<double><<<(unsigned)cdiv(d * d, 256), 256, 0, st>>>((double*)out, d, ldo);
   else
