@@ -15,6 +15,7 @@
 //      floating-point atomics, so SA is bitwise identical to the reference.
 // Algorithmic bytes: (n + m) * d * sizeof(T).
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "rng.cuh"
@@ -45,36 +46,52 @@ __global__ void __launch_bounds__(128) k_bucket_accumulate(
     double acc[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+    // entry indices of the next group are fetched one group ahead, so the row
+    // loads of a group do not wait behind their own index loads
+    int32_t en[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) en[u] = (p0 + u < p1) ? __ldg(order + p0 + u) : -1;
     for (int32_t p = p0; p < p1; p += UNROLL) {
+      int32_t ec[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) ec[u] = en[u];
       T a[UNROLL][VEC];
       int32_t sg[UNROLL];
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
-        if (p + u < p1) {
-          const int32_t e = order[p + u];          // entry index (row * s + t)
-          const int64_t row = e / sgn_stride;
-          sg[u] = sgn[e];
-          const T* src = A + row * lda + col0;
-          if (full && VEC > 1) {
-            if constexpr (VEC * sizeof(T) == 16) {
-              *reinterpret_cast<float4*>(a[u]) = __ldg(reinterpret_cast<const float4*>(src));
-            } else if constexpr (VEC * sizeof(T) == 8) {
-              *reinterpret_cast<float2*>(a[u]) = __ldg(reinterpret_cast<const float2*>(src));
-            } else {
+        const int32_t e = ec[u];  // entry index (row * s + t); -1 past the bucket
+        sg[u] = e >= 0 ? __ldg(sgn + e) : 0;
+        const int64_t row = e < 0 ? 0 : (sgn_stride == 1 ? e : e / sgn_stride);
+        const T* src = A + row * lda + col0;
+        if (e < 0) {
 #pragma unroll
-              for (int v = 0; v < VEC; ++v) a[u][v] = __ldg(src + v);
-            }
+          for (int v = 0; v < VEC; ++v) a[u][v] = (T)0;
+        } else if (full && VEC > 1) {
+          if constexpr (VEC == 2 && sizeof(T) == 8) {
+            const double2 t = __ldg(reinterpret_cast<const double2*>(src));
+            a[u][0] = (T)t.x;
+            a[u][VEC - 1] = (T)t.y;
+          } else if constexpr (VEC == 4 && sizeof(T) == 4) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+            a[u][0] = (T)t.x;
+            a[u][1 % VEC] = (T)t.y;
+            a[u][2 % VEC] = (T)t.z;
+            a[u][VEC - 1] = (T)t.w;
           } else {
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) a[u][v] = (col0 + v < d) ? __ldg(src + v) : (T)0;
+            for (int v = 0; v < VEC; ++v) a[u][v] = __ldg(src + v);
           }
         } else {
-          sg[u] = 0;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) a[u][v] = (col0 + v < d) ? __ldg(src + v) : (T)0;
         }
       }
+      const int32_t pn = p + UNROLL;
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) en[u] = (pn + u < p1) ? __ldg(order + pn + u) : -1;
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
-        if (p + u < p1) {
+        if (ec[u] >= 0) {
 #pragma unroll
           for (int v = 0; v < VEC; ++v) {
             double x = (double)a[u][v];
@@ -111,7 +128,16 @@ static int launch_accumulate(adask_ctx* ctx, const T* A, int64_t d, int64_t lda,
   const int threads = 128;
   const double scale = 1.0 / sqrt((double)s);
   const int use_scale = s > 1;
-  if (aligned) {
+  const int64_t narrow_below = getenv("ADASK_SJLT_NARROW") ? atoll(getenv("ADASK_SJLT_NARROW")) : 4 * kNumSMs;
+  if (m * cdiv(d, (int64_t)threads * VEC) < narrow_below) {
+    // few, long buckets: one thread per column and 16 rows in flight per
+    // thread (twice the threads and the same bytes in flight per thread)
+    int64_t panels = cdiv(d, (int64_t)threads);
+    int64_t gx = std::min<int64_t>(m, std::max<int64_t>(1, (int64_t)kNumSMs * 32 / panels));
+    dim3 grid((unsigned)gx, (unsigned)panels);
+    k_bucket_accumulate<T, 1, 16><<<grid, threads, 0, st>>>(A, d, lda, order, start, sgn, s, m, scale,
+                                                            use_scale, SA, ldsa, accumulate);
+  } else if (aligned) {
     int64_t panels = cdiv(d, (int64_t)threads * VEC);
     int64_t gx = std::min<int64_t>(m, std::max<int64_t>(1, (int64_t)kNumSMs * 32 / panels));
     dim3 grid((unsigned)gx, (unsigned)panels);

@@ -26,7 +26,7 @@ if which == "srht4":
 if which == "sjlt":
     n, d = 1 << 20, 2048
     A = torch.empty(n, d, dtype=torch.float64, device="cuda").normal_()
-    for m in (64, 2048, 65536):
+    for m in [int(x) for x in os.environ.get("MS", "64,2048,65536").split(",")]:
         ms = t(lambda: sjlt_dev(A, m, 7))
         print(f"sjlt n={n} d={d} m={m}: {ms*1e3:.1f} us  {(n+m)*d*8/ms/1e6:.0f} GB/s", flush=True)
 if which == "gauss":
