@@ -180,6 +180,37 @@ def philox_gaussian(m: int, n: int, seed: int, col0: int = 0) -> np.ndarray:
     return Z.reshape(4 * ngrp, n)[:m] / np.sqrt(m)
 
 
+def philox_gaussian_tf32(m: int, n: int, seed: int, col0: int = 0) -> np.ndarray:
+    """The TF32 tensor-core sketch's S (gauss_tc.cu, ADASK_TF32), restated:
+    for global column i and sketch-row octet g8 = k >> 3, Philox4x32-10 with
+    counter (i_lo, i_hi, g8, 0x54463332) and key = seed gives four words =
+    eight 16-bit halves h_0..h_7 (low half of word j is h_{2j});
+    u_t = (h_t + 1/2) 2^-16; (z_{2p}, z_{2p+1}) = sqrt(-2 ln u_{2p})
+    (cos, sin)(2 pi u_{2p+1}); S[k, i] = z_{k & 7} / sqrt(m)."""
+    key = (int(seed) & 0xFFFFFFFF, (int(seed) >> 32) & 0xFFFFFFFF)
+    ngrp = (m + 7) // 8
+    i = np.arange(col0, col0 + n, dtype=np.uint64)
+    g = np.arange(ngrp, dtype=np.uint64)
+    ctr = np.zeros((ngrp, n, 4), dtype=np.uint64)
+    ctr[..., 0] = (i & np.uint64(0xFFFFFFFF))[None, :]
+    ctr[..., 1] = (i >> np.uint64(32))[None, :]
+    ctr[..., 2] = g[:, None]
+    ctr[..., 3] = 0x54463332
+    o = philox4x32_10(ctr, key).astype(np.uint64)
+    h = np.empty((ngrp, n, 8), dtype=np.float64)
+    for j in range(4):
+        h[..., 2 * j] = (o[..., j] & np.uint64(0xFFFF)).astype(np.float64)
+        h[..., 2 * j + 1] = (o[..., j] >> np.uint64(16)).astype(np.float64)
+    u = (h + 0.5) * 2.0**-16
+    Z = np.empty((ngrp, 8, n))
+    for p in range(4):
+        rad = np.sqrt(-2.0 * np.log(u[..., 2 * p]))
+        th = 6.283185307179586 * u[..., 2 * p + 1]
+        Z[:, 2 * p] = rad * np.cos(th)
+        Z[:, 2 * p + 1] = rad * np.sin(th)
+    return Z.reshape(8 * ngrp, n)[:m] / np.sqrt(m)
+
+
 def sketch_gaussian(A: np.ndarray, m: int, seed: int, S: np.ndarray | None = None) -> np.ndarray:
     """embeddings.py:66-73 with the Philox S (or an injected S)."""
     A = np.asarray(A, dtype=np.float64)

@@ -186,7 +186,9 @@ def _tf32_case(n, d, m, row0, seed, accumulate=False):
     rng = np.random.default_rng(n + d + m)
     A = rng.standard_normal((n, d)).astype(np.float32)
     Ad = torch.from_numpy(A).cuda()
-    S = O.philox_gaussian(m, n, seed, col0=row0)
+    # the TF32 path has its own entry definition (16-bit uniforms); the FP32-pipe
+    # fallback (rows not 16-byte aligned) keeps the fp64 / fp32 definition
+    S = (O.philox_gaussian_tf32 if d % 4 == 0 else O.philox_gaussian)(m, n, seed, col0=row0)
     ref = S @ A.astype(np.float64)
     bound = np.abs(S) @ np.abs(A.astype(np.float64))
     base = None
