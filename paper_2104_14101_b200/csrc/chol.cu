@@ -102,6 +102,10 @@ int chol_factor_inverse(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t k
             "transpose %.1f us, total %.1f us\n", nb, (long long)k, (long long)kp, grid, diag, trsm, syrk,
             (tl[3 * nblk + 2] - tl[3 * nblk + 1]) * 1e-3, (tl[3 * nblk + 3] - tl[3 * nblk + 2]) * 1e-3,
             (tl[3 * nblk + 3] - tl[0]) * 1e-3);
+    fprintf(stderr, "[chol prologue] tile load %.2f us, diag factor %.2f us (pivots %.2f, inverse %.2f), store %.2f us\n",
+            (tl[3 * nblk + 4] - tl[0]) * 1e-3, (tl[3 * nblk + 5] - tl[3 * nblk + 4]) * 1e-3,
+            (tl[3 * nblk + 9] - tl[3 * nblk + 8]) * 1e-3, (tl[3 * nblk + 10] - tl[3 * nblk + 9]) * 1e-3,
+            (tl[3 * nblk + 6] - tl[3 * nblk + 5]) * 1e-3);
   }
   const int h = ctx->pinned_flags[0];
   if (info_host) *info_host = h;

@@ -11,6 +11,7 @@ struct CholArgs {
   int kp, nblk, k;
   int* info;
   unsigned long long* tlog;  // optional phase timestamps (ADASK_CHOL_TRACE)
+  int slow_diag;             // 1: unblocked pivot loop (ADASK_CHOL_SLOWDIAG, comparison)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -138,12 +139,67 @@ __device__ void build_tri_table(unsigned short* tab) {
 // warp w owns columns 8w..8w+7, lanes own rows lane and lane+32, finalized
 // rows broadcast by shuffles (no block barrier inside the loop).
 __device__ void diag_factor(double (*S)[NBP], double (*X)[NBP], const unsigned short* tab, int* info,
-                            int goff, int kvalid, unsigned long long* tl = nullptr) {
+                            int goff, int kvalid, unsigned long long* tl = nullptr, int slow = 0) {
   __shared__ double rinv[NB];
   if (tl && threadIdx.x == 0) tl[0] = gtimer2();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if constexpr (NB == 32) {
+    // Blocked pivot loop (same floating-point operations in the same order as
+    // the unblocked loop below, so the factor is bitwise the same): four panels
+    // of 8 pivots.  Warp 0 factors the 32 - jb rows of a panel in registers
+    // (lane = row; multipliers broadcast by shuffles, no block barrier per
+    // pivot); the whole CTA then applies the panel's 8 rank-1 updates to the
+    // trailing triangle, pivot by pivot for every element.
+    if (!slow) {
+#ifndef ADASK_CHOL_PW
+#define ADASK_CHOL_PW 8
+#endif
+      constexpr int PW = ADASK_CHOL_PW;  // panel width (pivots per warp-register panel)
 #pragma unroll 1
-  for (int j = 0; j < NB; ++j) {
+      for (int jb = 0; jb < NB; jb += PW) {
+        if (warp == 0) {
+          const unsigned FULL = 0xffffffffu;
+          const int i = jb + lane;
+          double r[PW];
+#pragma unroll
+          for (int q = 0; q < PW; ++q) r[q] = i < NB ? S[i][jb + q] : 0.0;
+#pragma unroll
+          for (int p = 0; p < PW; ++p) {
+            const double pj = __shfl_sync(FULL, r[p], p);
+            const double rd = rsqrt(pj);
+            if (lane == 0) {
+              if ((!(pj > 0.0) || !isfinite(pj)) && goff + jb + p < kvalid) atomicCAS(info, 0, goff + jb + p + 1);
+              rinv[jb + p] = rd;
+            }
+            const double l = lane > p ? r[p] * rd : (lane == p ? pj * rd : r[p]);
+            r[p] = l;
+#pragma unroll
+            for (int q = p + 1; q < PW; ++q) {
+              const double lq = __shfl_sync(FULL, l, q);
+              if (lane >= q) r[q] = fma(-l, lq, r[q]);
+            }
+          }
+          if (i < NB) {
+#pragma unroll
+            for (int q = 0; q < PW; ++q) S[i][jb + q] = r[q];
+          }
+        }
+        __syncthreads();
+        const int base = jb + PW, nt = NB - base;
+        for (int e = t; e < nt * nt; e += kCholThreads) {
+          const int ii = base + e / nt, ll = base + e % nt;
+          if (ll > ii) continue;
+          double v = S[ii][ll];
+#pragma unroll
+          for (int p = 0; p < PW; ++p) v = fma(-S[ii][jb + p], S[ll][jb + p], v);
+          S[ii][ll] = v;
+        }
+        __syncthreads();
+      }
+    }
+  }
+#pragma unroll 1
+  for (int j = 0; j < (NB == 32 && !slow ? 0 : NB); ++j) {
     const double pj = S[j][j];
     const double rd = rsqrt(pj);
     if (t > j && t < NB) S[t][j] *= rd;
@@ -233,7 +289,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
     tile_load<T>(sA, M, ld, 0, 0);
     __syncthreads();
     TMARK(3 * nblk + 4);
-    diag_factor(sA, sB, tri_tab, a.info, 0, a.k, a.tlog ? a.tlog + 3 * nblk + 8 : nullptr);
+    diag_factor(sA, sB, tri_tab, a.info, 0, a.k, a.tlog ? a.tlog + 3 * nblk + 8 : nullptr, a.slow_diag);
     TMARK(3 * nblk + 5);
     tile_store<T>(L, ld, 0, 0, sA, false, 1);
     tile_store<T>(Li, ld, 0, 0, sB, false, 1);
@@ -290,7 +346,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
       __syncthreads();
       if (t == 0) {
         // the updated diagonal tile j+1 is final: factor it now
-        diag_factor(sC, sB, tri_tab, a.info, (j + 1) * NB, a.k);
+        diag_factor(sC, sB, tri_tab, a.info, (j + 1) * NB, a.k, nullptr, a.slow_diag);
         tile_store<T>(L, ld, j + 1, j + 1, sC, false, 1);
         tile_store<T>(Li, ld, j + 1, j + 1, sB, false, 1);
       } else {
@@ -384,7 +440,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
 inline int launch(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, void* L, void* Li, void* LiT,
                   int* info, unsigned long long* tlog, cudaStream_t st, int* grid_out) {
   const int nblk = (int)(kp / NB);
-  CholArgs a{M, L, Li, LiT, (int)kp, nblk, (int)k, info, tlog};
+  CholArgs a{M, L, Li, LiT, (int)kp, nblk, (int)k, info, tlog, getenv("ADASK_CHOL_SLOWDIAG") ? 1 : 0};
   const int smem = 3 * NB * NBP * (int)sizeof(double);
   void* fn = dtype == ADASK_F64 ? (void*)k_chol_coop<double> : (void*)k_chol_coop<float>;
   ADASK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
