@@ -223,6 +223,55 @@ __device__ void diag_factor(double (*S)[NBP], double (*X)[NBP], const unsigned s
     if (j > i) S[i][j] = 0.0;
   }
   __syncthreads();
+  if constexpr (NB == 32) {
+    if (!slow) {
+      // X = L^-1 by 2 x 2 blocks of 16: the two diagonal blocks are inverted
+      // concurrently (warps 0-3 and 4-7, row-sequential as below but 16 steps),
+      // then X21 = -X22 (L21 X11) with two 16 x 16 x 16 products (X12 = 0 is
+      // the scratch for L21 X11)
+      const int half = warp >> 2, o = 16 * half, cw = o + (warp & 3) * 4;
+      double acc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = (o + lane == cw + q) ? 1.0 : 0.0;
+#pragma unroll 1
+      for (int i = 0; i < 16; ++i) {
+        const double ri = rinv[o + i];
+        double xi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double v = __shfl_sync(0xffffffffu, acc[q], i);
+          xi[q] = (cw + q <= o + i) ? v * ri : 0.0;
+        }
+        if (lane == i) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = xi[q];
+        }
+        const double lri = (lane > i && lane < 16) ? S[o + lane][o + i] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = fma(-lri, xi[q], acc[q]);
+      }
+      if (lane < 16) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) X[o + lane][cw + q] = acc[q];
+      }
+      __syncthreads();
+      const int rr = t >> 4, cc = t & 15;
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) sum = fma(S[16 + rr][k], X[k][cc], sum);
+      X[rr][16 + cc] = sum;  // (L21 X11)[rr][cc]
+      __syncthreads();
+      double u = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) u = fma(X[16 + rr][16 + k], X[k][16 + cc], u);
+      __syncthreads();
+      X[16 + rr][cc] = -u;
+      X[rr][16 + cc] = 0.0;
+      __syncthreads();
+      if (tl && threadIdx.x == 0) tl[2] = gtimer2();
+      return;
+    }
+  }
   constexpr int CPW = NB / 8;  // columns per warp
   constexpr int RPL = NB / 32; // rows per lane
   double acc[RPL][CPW];
