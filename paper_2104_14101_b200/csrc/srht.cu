@@ -297,6 +297,9 @@ static int fwht_select(adask_ctx* ctx, int dtype, const void* A, int64_t n, int6
                        cudaStream_t st) {
   const int L = ilog2(n_pad);
   int b1 = std::max(std::min(L, 10), L - 12);
+  // many slots (m >= 4096 of >= 2^20 rows): the 11-bit pass-1 tiles and the
+  // shorter pass 2 move the same intermediate ~10% faster (measured)
+  if (L >= 20 && m >= 4096) b1 = 11;
   if (const char* e = getenv("ADASK_FWHT_B1")) b1 = std::max(L - 12, std::min(L, atoi(e)));
   const int64_t B = 1ll << b1, G = n_pad >> b1;
   const int L2 = L - b1;
