@@ -340,6 +340,38 @@ def run_ours(args) -> None:
         ms = float(t.item())
     rel_err = ak.exact_error(p, x, sol) / d0
 
+    # ---- incremental sketch growth (north_star; not reference semantics): the
+    # same solve with the sketch grown instead of redrawn when m doubles
+    incr = None
+    if cfg.family != "sjlt" and not args.no_incremental and not sharded:
+        _log("incremental growth variant")
+        kw_i = dict(kw, incremental=True)
+        T_i = cfg.t_star + 2
+        t_i = None
+        for _ in range(4):
+            _, tr_i = ak.adaptive_run(p, x0, acfg_for(T_i), method=cfg.method, sol=sol, **kw_i)
+            d0_i = tr_i.records[0].delta_exact
+            t_i = next((r.t for r in tr_i.records if r.event != "resketch" and r.delta_exact <= cfg.target * d0_i),
+                       None)
+            if t_i is not None:
+                break
+            T_i = int(T_i * 1.5) + 1
+        t_i = t_i if t_i is not None else T_i
+        acfg_i = acfg_for(t_i)
+        for _ in range(args.warmup):
+            ak.adaptive_run(p, x0, acfg_i, method=cfg.method, **kw_i)
+        torch.cuda.synchronize()
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0.record()
+        for _ in range(args.steps):
+            x_i, tr_i = ak.adaptive_run(p, x0, acfg_i, method=cfg.method, **kw_i)
+        i1.record()
+        torch.cuda.synchronize()
+        incr = {"ms_per_step": i0.elapsed_time(i1) / args.steps, "T": t_i, "schedule": tr_i.schedule(),
+                "rel_err_final": ak.exact_error(p, x_i, sol) / d0_i,
+                "note": "sketch grown instead of redrawn at each resketch (SRHT: transform kept, rows added; "
+                        "Gaussian: rows kept and rescaled, new rows added); not the reference's draw sequence"}
+
     # ---- end to end through the public API from pinned host memory
     _log("e2e")
     e2e = _e2e(args, cfg, p, host_inst, acfg, kw, ws, dist, dev)
@@ -412,6 +444,7 @@ def run_ours(args) -> None:
                          "peak_source": pk["source"] + (" (bf16/2 for tf32)" if tensor else "")},
             "clocks": clk.summary(),
             "e2e": e2e,
+            "incremental": incr,
             "gpu_launches": int(launches),
             "cpu_baseline": cpu,
         }
@@ -491,6 +524,7 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tf32", action="store_true", help="fp32 Gaussian sketch on the FP32 pipe instead of TF32")
+    ap.add_argument("--no-incremental", action="store_true", help="skip the incremental-growth variant")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

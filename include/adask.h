@@ -56,6 +56,7 @@ enum adask_dtype { ADASK_F64 = 0, ADASK_F32 = 1 };
 #define ADASK_ACCUMULATE 0x1u /* sketch: SA += result instead of SA = result      */
 #define ADASK_PARTIAL 0x2u    /* hess_mult: out = A^T A X only (no nu^2 Lam X - B) */
 #define ADASK_TF32 0x4u       /* gaussian fp32: TF32 tensor-core GEMM             */
+#define ADASK_INCREMENTAL 0x8u /* adaptive_run: grow the sketch instead of redrawing */
 
 const char* adask_last_error(void);
 int adask_version(void);
@@ -161,6 +162,12 @@ int adask_philox_gaussian_host(int64_t m, int64_t col0, int64_t ncols, uint64_t 
 int adask_sketch_gaussian(adask_ctx* ctx, int dtype, const void* A, int64_t n_local, int64_t d,
                           int64_t lda, int64_t row0, int64_t m, uint64_t key, void* SA,
                           int64_t ldsa, uint32_t flags, void* stream);
+/* Rows [k0, k0 + mk) of the m_total-row Gaussian sketch (entries scaled by
+ * 1/sqrt(m_total)) into SA rows 0 .. mk-1: incremental sketch growth
+ * computes only the new rows when m doubles.                               */
+int adask_sketch_gaussian_rows(adask_ctx* ctx, int dtype, const void* A, int64_t n_local, int64_t d,
+                               int64_t lda, int64_t row0, int64_t m_total, int64_t k0, int64_t mk,
+                               uint64_t key, void* SA, int64_t ldsa, uint32_t flags, void* stream);
 
 /* SRHT: SA = Y[idx] * sqrt(n_pad/m), Y = fwht(diag(signs) A_padded)/sqrt(n_pad)
  * (embeddings.py:81-102, linalg.py:62-88).  `g` is the fresh generator of

@@ -451,6 +451,58 @@ class Trace:
         return [(r.t, r.m) for r in self.records if r.event == "resketch"]
 
 
+class IncrementalSketcher:
+    """The library's incremental sketch growth (driver.cu: make_sketch_incr),
+    restated: every sketch uses the seed of sketch 0 (derive_seed(seed, 0)).
+    Gaussian (Philox S, or the TF32 definition): the first sketch is S(m) A;
+    growing to m' keeps the rows as SA * sqrt(m / m') and appends rows
+    [m, m') of S(m') A.  SRHT / block SRHT: Y_b = fwht(D_b pad(A_b)) /
+    sqrt(n_pad_b) once per block (signs = integers(0, 2, n_b) of the block's
+    generator), perm_b = choice(n_pad_b, n_pad_b, replace=False) drawn next;
+    SA(m) = sum_b Y_b[perm_b[:m]] * sqrt(n_pad_b / m)."""
+
+    def __init__(self, family: str, seed: int, block: int | None = None, tf32: bool = False):
+        self.family, self.seed0, self.block, self.tf32 = family, derive_seed(seed, 0), block, tf32
+        self.SA = None
+        self.m = 0
+        self.Y = None
+
+    def __call__(self, A, m: int, _seed=None):
+        A = np.asarray(A, dtype=np.float64)
+        if self.family == "gaussian":
+            gen = philox_gaussian_tf32 if self.tf32 else philox_gaussian
+            if self.SA is None:
+                self.SA = gen(m, A.shape[0], self.seed0) @ A
+            elif m != self.m:
+                new = gen(m, A.shape[0], self.seed0)[self.m:] @ A
+                self.SA = np.vstack([self.SA * np.sqrt(self.m / m), new])
+            self.m = m
+            return self.SA.copy()
+        if self.family in ("srht", "srht-block"):
+            if self.Y is None:
+                n = A.shape[0]
+                B = n if self.family == "srht" else self.block
+                self.Y = []
+                for b, r0 in enumerate(range(0, n, B)):
+                    Ab = A[r0:r0 + B]
+                    nb = Ab.shape[0]
+                    npad = padded_rows(nb)
+                    sd = self.seed0 if self.family == "srht" else derive_seed(self.seed0, b)
+                    rng = np.random.default_rng(sd)
+                    bits = rng.integers(0, 2, size=nb)
+                    X = np.zeros((npad, Ab.shape[1]))
+                    X[:nb] = Ab * (bits * 2.0 - 1.0)[:, None]
+                    Y = fwht(X, normalized=True)
+                    perm = rng.choice(npad, size=npad, replace=False)
+                    self.Y.append((Y, perm, npad))
+            SA = None
+            for Y, perm, npad in self.Y:
+                part = Y[perm[:m]] * np.sqrt(npad / m)
+                SA = part if SA is None else SA + part
+            return SA
+        raise ValueError(f"no incremental rule for family {self.family!r}")
+
+
 def adaptive_run(p: Problem, x0, method: str, rho: float, m_init: int, T: int, family: str,
                  seed: int, s: int = 1, x_star=None, sketcher=None, cap=None, log=None):
     """solvers.py:585-659 (ihs / pcg).  `sketcher(A, m, seed)` replaces

@@ -20,6 +20,7 @@ E_DIM, E_NOT_SPD, E_NOT_POW2, E_SKETCH_TOO_LARGE, E_SPARSITY = 1, 2, 3, 4, 5
 E_NEGATIVE, E_BREAKDOWN, E_ARG, E_CUDA, E_NOMEM = 6, 7, 8, 9, 10
 F64, F32 = 0, 1
 ACCUMULATE, PARTIAL, TF32 = 0x1, 0x2, 0x4
+INCREMENTAL = 0x8
 
 _STATUS_EXC = {
     E_DIM: errors.DimensionMismatch,
@@ -124,6 +125,7 @@ _PROTOS = {
     "adask_philox_gaussian": (C.c_int, [vp, C.c_int, i64, i64, i64, u64, vp, i64, vp]),
     "adask_philox_gaussian_host": (C.c_int, [i64, i64, i64, u64, vp, i64]),
     "adask_sketch_gaussian": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, i64, i64, u64, vp, i64, u32, vp]),
+    "adask_sketch_gaussian_rows": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, i64, i64, i64, i64, u64, vp, i64, C.c_uint32, vp]),
     "adask_sketch_srht": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, P(PCG64State), i64, vp, i64, P(i64), u32, vp]),
     "adask_sketch_sjlt": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, i64, i64, i64, i64, P(PCG64State),
                                     P(i64), u64, vp, i64, u32, vp]),

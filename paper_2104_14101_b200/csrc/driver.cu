@@ -113,6 +113,105 @@ static int make_sketch(adask_ctx* ctx, const adask_problem* pb, const adask_adap
   return ADASK_OK;
 }
 
+// ------------------------------------------------------------ incremental growth
+// ADASK_INCREMENTAL: every sketch uses the seed of sketch 0 and the sketch
+// grows instead of being redrawn when m doubles (north_star "incremental
+// sketch growth"; not reference semantics, so the oracle has the same mode).
+//   Gaussian: rows [0, m_old) are the previous SA rescaled by sqrt(m_old / m),
+//             only rows [m_old, m) are generated and applied;
+//   SRHT / block SRHT: the normalized transform Y = fwht(D A) / sqrt(n_pad)
+//             of every block is computed once and kept; a sketch of any m is
+//             the gather Y[perm[:m]] * sqrt(n_pad / m) (nested uniform subsets);
+//   SJLT: redrawn as in the reference mode.
+template <typename T>
+__global__ void k_rescale_rows(const T* __restrict__ src, int64_t n, double s, T* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = (T)((double)src[i] * s);
+}
+
+struct Incremental {
+  bool on = false;
+  DevBuf ybuf, pbuf;          // transforms of all blocks, draw orders
+  std::vector<int64_t> npad;  // per block
+  std::vector<size_t> yoff, poff;
+  bool ready = false;
+};
+
+static int make_sketch_incr(adask_ctx* ctx, const adask_problem* pb, const adask_adaptive_cfg* cfg, Incremental& inc,
+                            int64_t m, const void* SA_old, int64_t m_old, void* SA, cudaStream_t st) {
+  const int64_t d = pb->d;
+  const size_t esz = pb->dtype == ADASK_F64 ? 8 : 4;
+  const uint64_t seed0 = adask_derive_seed(cfg->seed, 0);
+  if (cfg->family == ADASK_GAUSSIAN) {
+    if (!SA_old || m_old <= 0) {
+      ADASK_TRY(adask_sketch_gaussian(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, cfg->row0, m, seed0, SA, d,
+                                      cfg->flags & ADASK_TF32, (void*)st));
+      if (pb->allreduce && pb->allreduce(SA, m * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
+        return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
+      return ADASK_OK;
+    }
+    if (m == m_old) {  // capped retry: the grown sketch is the same sketch
+      ADASK_CUDA(cudaMemcpyAsync(SA, SA_old, (size_t)m * d * esz, cudaMemcpyDeviceToDevice, st));
+      return ADASK_OK;
+    }
+    const double sc = std::sqrt((double)m_old / (double)m);
+    const int64_t nold = m_old * d;
+    if (pb->dtype == ADASK_F64)
+      k_rescale_rows<double><<<(unsigned)cdiv(nold, 256), 256, 0, st>>>((const double*)SA_old, nold, sc, (double*)SA);
+    else
+      k_rescale_rows<float><<<(unsigned)cdiv(nold, 256), 256, 0, st>>>((const float*)SA_old, nold, sc, (float*)SA);
+    ADASK_LAUNCHED(ctx);
+    void* fresh = (char*)SA + (size_t)nold * esz;
+    ADASK_TRY(adask_sketch_gaussian_rows(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, cfg->row0, m, m_old, m - m_old,
+                                         seed0, fresh, d, cfg->flags & ADASK_TF32, (void*)st));
+    if (pb->allreduce && pb->allreduce(fresh, (m - m_old) * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
+      return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
+    return ADASK_OK;
+  }
+  if (cfg->family == ADASK_SRHT || cfg->family == ADASK_SRHT_BLOCK) {
+    const bool blocked = cfg->family == ADASK_SRHT_BLOCK;
+    const int64_t B = blocked ? cfg->block : pb->n;
+    if (!blocked && cfg->n_total != pb->n) return fail(ADASK_E_ARG, "the global SRHT does not shard (use block SRHT)");
+    if (blocked && (B < 1 || cfg->row0 % B)) return fail(ADASK_E_ARG, "block SRHT: shard must start on a block boundary");
+    if (!inc.ready) {
+      size_t ybytes = 0, pcount = 0;
+      for (int64_t r0 = 0; r0 < pb->n; r0 += B) {
+        const int64_t rows = std::min<int64_t>(B, pb->n - r0);
+        const int64_t np = (int64_t)1 << (int)std::ceil(std::log2((double)std::max<int64_t>(rows, 1)));
+        inc.npad.push_back(np);
+        inc.yoff.push_back(ybytes);
+        inc.poff.push_back(pcount);
+        ybytes += (size_t)np * d * esz;
+        pcount += (size_t)np;
+      }
+      ADASK_TRY(inc.ybuf.alloc(ybytes, st));
+      ADASK_TRY(inc.pbuf.alloc(pcount * sizeof(int64_t), st));
+      std::vector<int64_t> perm;
+      size_t bi = 0;
+      for (int64_t r0 = 0; r0 < pb->n; r0 += B, ++bi) {
+        const int64_t rows = std::min<int64_t>(B, pb->n - r0);
+        adask_pcg64 g;
+        ADASK_TRY(gen_from_seed(blocked ? adask_derive_seed(seed0, (uint64_t)((cfg->row0 + r0) / B)) : seed0, &g));
+        perm.assign((size_t)inc.npad[bi], 0);
+        const void* Ab = (const char*)pb->A + (size_t)r0 * pb->lda * esz;
+        ADASK_TRY(srht_transform_impl(ctx, pb->dtype, Ab, rows, d, pb->lda, &g, (char*)inc.ybuf.p + inc.yoff[bi],
+                                      perm.data(), st));
+        ADASK_CUDA(cudaMemcpyAsync((int64_t*)inc.pbuf.p + inc.poff[bi], perm.data(), perm.size() * sizeof(int64_t),
+                                   cudaMemcpyHostToDevice, st));
+        ADASK_CUDA(cudaStreamSynchronize(st));  // perm (pageable host) is reused by the next block
+      }
+      inc.ready = true;
+    }
+    for (size_t bi = 0; bi < inc.npad.size(); ++bi)
+      ADASK_TRY(srht_gather_impl(ctx, pb->dtype, (char*)inc.ybuf.p + inc.yoff[bi], inc.npad[bi], d,
+                                 (const int64_t*)inc.pbuf.p + inc.poff[bi], m, SA, d, bi > 0 ? 1 : 0, st));
+    if (pb->allreduce && pb->allreduce(SA, m * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
+      return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
+    return ADASK_OK;
+  }
+  return make_sketch(ctx, pb, cfg, m, seed0, SA, st);  // SJLT: no growth rule, redraw
+}
+
 static int exact_err(adask_ctx* ctx, const adask_problem* pb, const double* x, const double* xstar,
                      double* diff, double* Hd, double* out, cudaStream_t st) {
   const int64_t n = pb->d * pb->c;
@@ -183,7 +282,12 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
   // sketch + build
   DevBuf sa_buf;
   ADASK_TRY(sa_buf.alloc((size_t)m * d * esz, st));
-  ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, 0), sa_buf.p, st));
+  Incremental inc;
+  inc.on = (cfg->flags & ADASK_INCREMENTAL) != 0;
+  if (inc.on)
+    ADASK_TRY(make_sketch_incr(ctx, pb, cfg, inc, m, nullptr, 0, sa_buf.p, st));
+  else
+    ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, 0), sa_buf.p, st));
   adask_precond* P = nullptr;
   int64_t info = 0;
   ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
@@ -232,13 +336,17 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
     if (reject) {
       K += 1;
       const bool at_cap = m >= cap;
+      const int64_t m_old = m;
       m = std::min(2 * m, cap);
       capped_retry = at_cap;
       adask_precond_destroy(P);
       P = nullptr;
       DevBuf nsa;
       ADASK_TRY(nsa.alloc((size_t)m * d * esz, st));
-      ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, (uint64_t)K), nsa.p, st));
+      if (inc.on)
+        ADASK_TRY(make_sketch_incr(ctx, pb, cfg, inc, m, sa_buf.p, m_old, nsa.p, st));
+      else
+        ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, (uint64_t)K), nsa.p, st));
       std::swap(sa_buf.p, nsa.p);  // the previous SA is released (stream-ordered) with nsa
       ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
                                     (void*)st));

@@ -14,52 +14,59 @@ namespace adask {
 
 int gauss_tc_impl(adask_ctx* ctx, const float* A, int64_t n_local, int64_t d, int64_t lda,
                   int64_t row0, int64_t m, uint64_t key, float* SA, int64_t ldsa, bool accumulate,
-                  cudaStream_t st);
+                  cudaStream_t st, int64_t kg0, int64_t m_total);
 
 }  // namespace adask
 
 using namespace adask;
 
-extern "C" int adask_sketch_gaussian(adask_ctx* ctx, int dtype, const void* A, int64_t n_local,
-                                     int64_t d, int64_t lda, int64_t row0, int64_t m, uint64_t key,
-                                     void* SA, int64_t ldsa, uint32_t flags, void* stream) {
+// Rows [k0, k0 + mk) of the m_total-row sketch (S scaled by 1/sqrt(m_total)),
+// written to SA rows 0 .. mk-1.  adask_sketch_gaussian is k0 = 0, mk = m_total;
+// incremental growth (driver.cu) computes only the new rows.
+extern "C" int adask_sketch_gaussian_rows(adask_ctx* ctx, int dtype, const void* A, int64_t n_local, int64_t d,
+                                          int64_t lda, int64_t row0, int64_t m_total, int64_t k0, int64_t mk,
+                                          uint64_t key, void* SA, int64_t ldsa, uint32_t flags, void* stream) {
   ADASK_TRY(use_device(ctx));
-  if (m < 1) return fail(ADASK_E_SKETCH_TOO_LARGE, "sketch size must be a positive integer, got %lld",
-                         (long long)m);
+  if (m_total < 1 || mk < 1 || k0 < 0 || k0 + mk > m_total)
+    return fail(ADASK_E_SKETCH_TOO_LARGE, "sketch rows [%lld, %lld) of m = %lld", (long long)k0,
+                (long long)(k0 + mk), (long long)m_total);
   if (n_local < 0 || d < 1 || lda < d || ldsa < d || row0 < 0)
     return fail(ADASK_E_DIM, "sketch_gaussian: bad shape");
   if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
   cudaStream_t st = S(stream);
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
   const bool accumulate = (flags & ADASK_ACCUMULATE) != 0;
-  ProfScope prof(ctx, PK_GAUSS, st, (double)n_local * d * esz, 2.0 * (double)m * n_local * d);
-  // tcgen05 path needs 16-byte aligned rows (TMA); otherwise the FP32-pipe GEMM
-  if ((flags & ADASK_TF32) && dtype == ADASK_F32 && lda % 4 == 0 && ((uintptr_t)A & 15) == 0) {
-    return gauss_tc_impl(ctx, (const float*)A, n_local, d, lda, row0, m, key, (float*)SA, ldsa,
-                         accumulate, st);
+  ProfScope prof(ctx, PK_GAUSS, st, (double)n_local * d * esz, 2.0 * (double)mk * n_local * d);
+  // tcgen05 path needs 16-byte aligned rows (TMA) and an octet-aligned row offset; otherwise the FP32-pipe GEMM
+  if ((flags & ADASK_TF32) && dtype == ADASK_F32 && lda % 4 == 0 && ((uintptr_t)A & 15) == 0 && k0 % 8 == 0) {
+    return gauss_tc_impl(ctx, (const float*)A, n_local, d, lda, row0, mk, key, (float*)SA, ldsa, accumulate, st,
+                         k0, m_total);
   }
   if (n_local == 0) {
-    if (!accumulate) ADASK_CUDA(cudaMemset2DAsync(SA, ldsa * esz, 0, d * esz, m, st));
+    if (!accumulate) ADASK_CUDA(cudaMemset2DAsync(SA, ldsa * esz, 0, d * esz, mk, st));
     return ADASK_OK;
   }
   // chunk of S columns (rows of A) so that S_chunk stays <= 256 MiB
-  int64_t nc = (int64_t)((256ll << 20) / ((int64_t)m * (int64_t)esz));
+  int64_t nc = (int64_t)((256ll << 20) / ((int64_t)mk * (int64_t)esz));
   nc = std::max<int64_t>(256, nc / 256 * 256);
   nc = std::min<int64_t>(nc, n_local);
   void* wsp = nullptr;
-  ADASK_TRY(ctx->ws[WS_GAUSS].get((size_t)m * nc * esz, st, &wsp));
-  const double sc = sqrt((double)m);
-  const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+  ADASK_TRY(ctx->ws[WS_GAUSS].get((size_t)mk * nc * esz, st, &wsp));
   for (int64_t c0 = 0; c0 < n_local; c0 += nc) {
     const int64_t w = std::min<int64_t>(nc, n_local - c0);
-    ADASK_TRY(adask_philox_gaussian(ctx, dtype, m, row0 + c0, w, key, wsp, w, stream));
+    ADASK_TRY(philox_gaussian_rows(ctx, dtype, k0, mk, m_total, row0 + c0, w, key, wsp, w, st));
     const void* Ac = (const char*)A + (size_t)c0 * lda * esz;
     const double beta = (c0 > 0 || accumulate) ? 1.0 : 0.0;
-    ADASK_TRY(gemm_impl(ctx, dtype, m, d, w, 1.0, wsp, w, false, Ac, lda, false, nullptr, beta, SA,
-                        ldsa, 0.0, nullptr, false, st));
+    ADASK_TRY(gemm_impl(ctx, dtype, mk, d, w, 1.0, wsp, w, false, Ac, lda, false, nullptr, beta, SA, ldsa, 0.0,
+                        nullptr, false, st));
   }
-  (void)sc;
-  (void)k0;
-  (void)k1;
   return ADASK_OK;
+}
+
+extern "C" int adask_sketch_gaussian(adask_ctx* ctx, int dtype, const void* A, int64_t n_local,
+                                     int64_t d, int64_t lda, int64_t row0, int64_t m, uint64_t key,
+                                     void* SA, int64_t ldsa, uint32_t flags, void* stream) {
+  if (m < 1) return fail(ADASK_E_SKETCH_TOO_LARGE, "sketch size must be a positive integer, got %lld",
+                         (long long)m);
+  return adask_sketch_gaussian_rows(ctx, dtype, A, n_local, d, lda, row0, m, 0, m, key, SA, ldsa, flags, stream);
 }

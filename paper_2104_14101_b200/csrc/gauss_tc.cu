@@ -159,7 +159,7 @@ template <int NH>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gauss_tc(const __grid_constant__ CUtensorMap amap, int64_t n_local, int64_t d, int64_t row0, int64_t m,
                uint32_t key0, uint32_t key1, float scale, int64_t k_per_slice, int m_pairs, int n_tiles,
-               float* __restrict__ out, int64_t ldo, int64_t slice_stride, int vec_ok, int dbg) {
+               float* __restrict__ out, int64_t ldo, int64_t slice_stride, int vec_ok, int64_t kg0, int dbg) {
   using C = TcCfg<NH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int gt = threadIdx.x - 64;  // 0 .. 32 NGEN - 1
     const int ro = gt & 15;           // tile rows 8 ro .. 8 ro + 7
     const int kk = gt >> 4;           // stage row
-    const uint32_t grp8 = (uint32_t)((m0 >> 3) + ro);
+    const uint32_t grp8 = (uint32_t)(((kg0 + m0) >> 3) + ro);  // global sketch-row octet
     uint32_t rk0[10], rk1[10];
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
@@ -381,14 +381,14 @@ __global__ void k_slice_sum(const float* __restrict__ P, int slices, int64_t sli
 template <int NH>
 int launch_tc(adask_ctx* ctx, const CUtensorMap& map, int64_t n_local, int64_t d, int64_t row0, int64_t m,
               uint64_t key, int64_t k_per_slice, int m_pairs, int n_tiles, int slices, float* out, int64_t ldo,
-              int64_t slice_stride, cudaStream_t st) {
+              int64_t slice_stride, int64_t kg0, int64_t m_total, cudaStream_t st) {
   using C = TcCfg<NH>;
   static bool attr = false;
   if (!attr) {
     ADASK_CUDA(cudaFuncSetAttribute(k_gauss_tc<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  const float scale = (float)(1.0 / sqrt((double)m));
+  const float scale = (float)(1.0 / sqrt((double)m_total));
   const int vec_ok = (ldo % 4 == 0) && (((uintptr_t)out & 15) == 0);
   const int dbg = getenv("ADASK_TC_DEBUG") ? atoi(getenv("ADASK_TC_DEBUG")) : 0;
   cudaLaunchConfig_t lc = {};
@@ -404,15 +404,18 @@ int launch_tc(adask_ctx* ctx, const CUtensorMap& map, int64_t n_local, int64_t d
   lc.attrs = at;
   lc.numAttrs = 1;
   ADASK_CUDA(cudaLaunchKernelEx(&lc, k_gauss_tc<NH>, map, n_local, d, row0, m, (uint32_t)key, (uint32_t)(key >> 32),
-                                scale, k_per_slice, m_pairs, n_tiles, out, ldo, slice_stride, vec_ok, dbg));
+                                scale, k_per_slice, m_pairs, n_tiles, out, ldo, slice_stride, vec_ok, kg0, dbg));
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;
 }
 
 }  // namespace
 
+// Rows [kg0, kg0 + m) of the m_total-row TF32 sketch (kg0 a multiple of 8).
 int gauss_tc_impl(adask_ctx* ctx, const float* A, int64_t n_local, int64_t d, int64_t lda, int64_t row0,
-                  int64_t m, uint64_t key, float* SA, int64_t ldsa, bool accumulate, cudaStream_t st) {
+                  int64_t m, uint64_t key, float* SA, int64_t ldsa, bool accumulate, cudaStream_t st, int64_t kg0,
+                  int64_t m_total) {
+  if (kg0 % 8 != 0) return fail(ADASK_E_ARG, "TF32 Gaussian sketch: row offset must be a multiple of 8");
   if (n_local == 0) {
     if (!accumulate) ADASK_CUDA(cudaMemset2DAsync(SA, ldsa * 4, 0, d * 4, m, st));
     return ADASK_OK;
@@ -453,10 +456,10 @@ int gauss_tc_impl(adask_ctx* ctx, const float* A, int64_t n_local, int64_t d, in
   }
   if (NH == 2)
     ADASK_TRY(launch_tc<2>(ctx, map, n_local, d, row0, m, key, k_per_slice, m_pairs, n_tiles, slices, out, ldo,
-                           slice_stride, st));
+                           slice_stride, kg0, m_total, st));
   else
     ADASK_TRY(launch_tc<1>(ctx, map, n_local, d, row0, m, key, k_per_slice, m_pairs, n_tiles, slices, out, ldo,
-                           slice_stride, st));
+                           slice_stride, kg0, m_total, st));
   if (out != SA) {
     const int64_t total = m * d;
     const int blocks = (int)std::min<int64_t>(cdiv(total, 256), 4 * kNumSMs);

@@ -181,10 +181,11 @@ int pcg_integers_impl(adask_ctx* ctx, const adask_pcg64* g, uint64_t first, int6
 
 // ---------------------------------------------------------------- Philox normals
 template <typename T>
-__global__ void k_philox_gaussian(int64_t m, int64_t col0, int64_t ncols, uint32_t k0, uint32_t k1,
+__global__ void k_philox_gaussian(int64_t krow0, int64_t mk, int64_t col0, int64_t ncols, uint32_t k0, uint32_t k1,
                                   double sc, T* __restrict__ out, int64_t ldo) {
-  // one thread per (column, group of four sketch rows); grid.y tiles groups
-  const int64_t g = blockIdx.y;
+  // one thread per (column, group of four global sketch rows); grid.y tiles
+  // the groups covering rows [krow0, krow0 + mk)
+  const int64_t g = (krow0 >> 2) + blockIdx.y;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncols) return;
   double z[4];
@@ -192,8 +193,25 @@ __global__ void k_philox_gaussian(int64_t m, int64_t col0, int64_t ncols, uint32
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int64_t k = 4 * g + q;
-    if (k < m) out[k * ldo + c] = (T)(z[q] / sc);
+    if (k >= krow0 && k < krow0 + mk) out[(k - krow0) * ldo + c] = (T)(z[q] / sc);
   }
+}
+
+// Rows [krow0, krow0 + mk) of the m_total-row Gaussian S (scale 1/sqrt(m_total)).
+int philox_gaussian_rows(adask_ctx* ctx, int dtype, int64_t krow0, int64_t mk, int64_t m_total, int64_t col0,
+                         int64_t ncols, uint64_t key, void* out, int64_t ldo, cudaStream_t st) {
+  if (mk <= 0 || ncols <= 0) return ADASK_OK;
+  const int64_t groups = ((krow0 + mk - 1) >> 2) - (krow0 >> 2) + 1;
+  if (groups > 65535) return fail(ADASK_E_ARG, "philox_gaussian: more than 262140 rows per call");
+  dim3 grid((unsigned)cdiv(ncols, 256), (unsigned)groups);
+  const double sc = sqrt((double)m_total);
+  const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+  if (dtype == ADASK_F64)
+    k_philox_gaussian<double><<<grid, 256, 0, st>>>(krow0, mk, col0, ncols, k0, k1, sc, (double*)out, ldo);
+  else
+    k_philox_gaussian<float><<<grid, 256, 0, st>>>(krow0, mk, col0, ncols, k0, k1, sc, (float*)out, ldo);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
 }
 
 }  // namespace adask
@@ -214,18 +232,7 @@ extern "C" int adask_philox_gaussian(adask_ctx* ctx, int dtype, int64_t m, int64
   if (m <= 0 || ncols < 0 || col0 < 0 || ldo < ncols || !out)
     return fail(ADASK_E_ARG, "philox_gaussian: bad arguments");
   if (ncols == 0) return ADASK_OK;
-  if (m > 4 * 65535) return fail(ADASK_E_ARG, "philox_gaussian: m > 262140 per call");
-  dim3 grid((unsigned)cdiv(ncols, 256), (unsigned)cdiv(m, 4));
-  double sc = sqrt((double)m);
-  uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
-  if (dtype == ADASK_F64)
-    k_philox_gaussian<double><<<grid, 256, 0, S(stream)>>>(m, col0, ncols, k0, k1, sc,
-                                                           (double*)out, ldo);
-  else
-    k_philox_gaussian<float><<<grid, 256, 0, S(stream)>>>(m, col0, ncols, k0, k1, sc,
-                                                          (float*)out, ldo);
-  ADASK_LAUNCHED(ctx);
-  return ADASK_OK;
+  return philox_gaussian_rows(ctx, dtype, 0, m, m, col0, ncols, key, out, ldo, S(stream));
 }
 
 // Host evaluation of the Gaussian entry definition (for CPU-side pinning of

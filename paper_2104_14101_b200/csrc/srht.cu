@@ -419,6 +419,60 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
                      (flags & ADASK_ACCUMULATE) ? 1 : 0, st);
 }
 
+// ---------------------------------------------------- incremental sketch growth
+// Y = fwht(diag(signs) pad(A)) / sqrt(n_pad) for every padded row (the
+// reference's intermediate Y, embeddings.py:97-99), kept resident so that an
+// m-row SRHT at the same seed is a gather Y[perm[:m]] * sqrt(n_pad / m).
+// perm = choice(n_pad, n_pad, replace=False) drawn right after the n sign
+// draws, so perm[:m] is a uniform m-subset for every m and the subsets are
+// nested as m doubles.
+int srht_transform_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                        const adask_pcg64* g, void* Y, int64_t* perm_host, cudaStream_t st) {
+  if (n < 1 || d < 1 || lda < d) return fail(ADASK_E_DIM, "srht_transform: bad shape");
+  const int64_t n_pad = 1ll << ilog2(n);
+  if (ilog2(n_pad) > 24) return fail(ADASK_E_ARG, "srht_transform: n_pad > 2^24 unsupported");
+  ProfScope prof(ctx, PK_SRHT, st, (double)(n + n_pad) * d * (dtype == ADASK_F64 ? 8 : 4));
+  void* sw = nullptr;
+  ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(n, 32) * 4 + 16, st, &sw));
+  uint32_t* sgn = (uint32_t*)sw;
+  ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
+  if (perm_host) {
+    adask_pcg64 h = *g;
+    adask_pcg64_skip_u32(&h, (uint64_t)n);
+    ADASK_TRY(adask_choice_noreplace(&h, n_pad, n_pad, perm_host));
+  }
+  return fwht_select(ctx, dtype, A, n, d, lda, sgn, n_pad, nullptr, n_pad, Y, d, sqrt((double)n_pad), 0.0, 0, st);
+}
+
+template <typename T>
+__global__ void k_gather_rows(const T* __restrict__ Y, int64_t d, const int64_t* __restrict__ perm, int64_t m,
+                              double scale, T* __restrict__ SA, int64_t ldsa, int accumulate) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * d) return;
+  const int64_t k = e / d, j = e - k * d;
+  const T y = (T)((double)Y[perm[k] * d + j] * scale);
+  T* o = SA + k * ldsa + j;
+  *o = accumulate ? (T)(*o + y) : y;
+}
+
+// SA (+)= Y[perm[:m]] * sqrt(n_pad / m)  (the reference's second scaling step)
+int srht_gather_impl(adask_ctx* ctx, int dtype, const void* Y, int64_t n_pad, int64_t d, const int64_t* perm_dev,
+                     int64_t m, void* SA, int64_t ldsa, int accumulate, cudaStream_t st) {
+  if (m > n_pad) return fail(ADASK_E_SKETCH_TOO_LARGE, "m = %lld exceeds padded row count %lld", (long long)m,
+                             (long long)n_pad);
+  ProfScope prof(ctx, PK_SRHT, st, (double)2 * m * d * (dtype == ADASK_F64 ? 8 : 4));
+  const double scale = sqrt((double)n_pad / (double)m);
+  const unsigned blocks = (unsigned)cdiv(m * d, 256);
+  if (dtype == ADASK_F64)
+    k_gather_rows<double><<<blocks, 256, 0, st>>>((const double*)Y, d, perm_dev, m, scale, (double*)SA, ldsa,
+                                                  accumulate);
+  else
+    k_gather_rows<float><<<blocks, 256, 0, st>>>((const float*)Y, d, perm_dev, m, scale, (float*)SA, ldsa,
+                                                 accumulate);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
 }  // namespace adask
 
 using namespace adask;

@@ -5,4 +5,11 @@ namespace adask {
 int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                      const adask_pcg64* g, int64_t m, void* SA, int64_t ldsa, int64_t* idx_host,
                      uint32_t flags, cudaStream_t st);
+// Incremental growth: the full normalized transform Y (n_pad x d, ld d) at
+// the generator's signs, and the draw order perm (n_pad entries, host);
+// then SA (+)= Y[perm[:m]] sqrt(n_pad / m).
+int srht_transform_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                        const adask_pcg64* g, void* Y, int64_t* perm_host, cudaStream_t st);
+int srht_gather_impl(adask_ctx* ctx, int dtype, const void* Y, int64_t n_pad, int64_t d, const int64_t* perm_dev,
+                     int64_t m, void* SA, int64_t ldsa, int accumulate, cudaStream_t st);
 }  // namespace adask

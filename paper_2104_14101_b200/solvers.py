@@ -431,7 +431,7 @@ _EVENTS = ("plain", "accepted", "resketch")
 
 
 def _adaptive_native(p: RegularizedProblem, x0, cfg: AdaptiveConfig, method: str, sol, tf32: bool,
-                     block: int):
+                     block: int, incremental: bool = False):
     """The same algorithm as the Python loop below, run by libadask's native
     driver (adask_adaptive_run): no Python / ctypes round trips per pass."""
     Xt, vec = _promote(p, x0)
@@ -442,7 +442,7 @@ def _adaptive_native(p: RegularizedProblem, x0, cfg: AdaptiveConfig, method: str
     c.rho, c.m_init, c.T, c.seed, c.s = float(cfg.rho), int(cfg.m_init), int(cfg.T), int(cfg.seed), int(cfg.s)
     c.alpha, c.phi_rho, c.c_alpha_rho = float(cfg.alpha), float(cfg.phi_rho), float(cfg.c_alpha_rho)
     c.block, c.row0, c.n_total = int(block), int(p.row0), int(p.n_total)
-    c.flags = _lib.TF32 if tf32 else 0
+    c.flags = (_lib.TF32 if tf32 else 0) | (_lib.INCREMENTAL if incremental else 0)
     if method == "polyak":
         c.phi_rho = 0.0  # the polyak threshold is evaluated on the host (see below)
     nmax = 3 * int(cfg.T) + 200
@@ -463,13 +463,18 @@ def _adaptive_native(p: RegularizedProblem, x0, cfg: AdaptiveConfig, method: str
 
 def adaptive_run(p: RegularizedProblem, x0, cfg: AdaptiveConfig, method: str = "pcg",
                  sol: ExactSolution | None = None, experimental: bool = False, *,
-                 tf32: bool = False, sketcher=None, block: int = 1 << 21, native: bool | None = None):
+                 tf32: bool = False, sketcher=None, block: int = 1 << 21, native: bool | None = None,
+                 incremental: bool = False):
     """Run a sketched method with on-line sketch-size adaptation
     (solvers.py:585-659).  Keyword-only extras: tf32 (fp32 Gaussian sketch on
     tensor cores), block (rows per block for family "srht-block", config 4),
     sketcher(p, spec) -> SA device tensor (custom sketches; forces the Python
     loop), native (default: the libadask driver whenever no custom sketcher
-    is given; set ADASK_PY_DRIVER=1 to force the Python loop)."""
+    is given; set ADASK_PY_DRIVER=1 to force the Python loop), incremental
+    (grow the sketch when m doubles instead of redrawing it: Gaussian keeps
+    its rows and adds new ones, SRHT keeps its transform and adds sampled
+    rows; not reference semantics -- the oracle's adaptive_run has the same
+    mode -- native driver only)."""
     if method not in _METHODS:
         raise ValueError(f"unknown method {method!r}; expected one of {_METHODS}")
     if method == "polyak" and not experimental:
@@ -477,6 +482,10 @@ def adaptive_run(p: RegularizedProblem, x0, cfg: AdaptiveConfig, method: str = "
     if native is None:
         native = (sketcher is None and method != "polyak" and 0 <= int(cfg.seed) < 2**64
                   and cfg.family in _FAMILY_CODE and os.environ.get("ADASK_PY_DRIVER") != "1")
+    if incremental:
+        if sketcher is not None or method == "polyak":
+            raise ValueError("incremental sketch growth runs on the native driver (no custom sketcher / polyak)")
+        return _adaptive_native(p, x0, cfg, method, sol, tf32, block, incremental=True)
     if native:
         return _adaptive_native(p, x0, cfg, method, sol, tf32, block)
     if sketcher is None and cfg.family == "srht-block":

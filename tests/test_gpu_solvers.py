@@ -200,3 +200,52 @@ def test_tri_solve_matches_scipy(k, c, transposed):
     np.testing.assert_allclose(got, ref, rtol=1e-10, atol=1e-12)
     with pytest.raises(ak.DimensionMismatch):
         ak.tri_solve(L, np.ones(k + 1))
+
+
+# ------------------------------------------------------------ incremental sketch growth
+@pytest.mark.parametrize("family,method,dtype", [("srht", "pcg", "float64"), ("gaussian", "ihs", "float64"),
+                                                 ("srht-block", "pcg", "float64"), ("gaussian", "ihs", "float32")])
+def test_incremental_growth_matches_oracle(family, method, dtype):
+    import paper_2104_14101_b200 as ak
+
+    rng = np.random.default_rng(4)
+    n, d = 3000, 60
+    A = rng.standard_normal((n, d)) / np.sqrt(n) * (0.9 ** np.arange(d))
+    b = A.T @ (A @ rng.standard_normal(d) + 0.01 * rng.standard_normal(n))
+    nu, T, seed, m0 = 0.05, 8, 3, 4
+    block = 1024
+    A_used = A.astype(np.float32).astype(np.float64) if dtype == "float32" else A
+    p = ak.RegularizedProblem(A, b, nu, dtype=dtype)
+    cfg = ak.AdaptiveConfig.for_method(method, 0.125, m0, T, family, seed)
+    x, tr = ak.adaptive_run(p, np.zeros(d), cfg, method=method, incremental=True, block=block)
+    po = O.Problem.make(A_used, b, nu, np.ones(d))
+    sk = O.IncrementalSketcher(family, seed, block=block)
+    cap = O.padded_rows(n) if family == "srht" else (min(n, O.padded_rows(block)) if family == "srht-block" else n)
+    xo, tro = O.adaptive_run(po, np.zeros(d), method, 0.125, m0, T, "srht" if family != "gaussian" else family,
+                             seed, sketcher=sk, cap=cap)
+    assert tr.schedule() == tro.schedule()
+    tol = 1e-4 if dtype == "float32" else 1e-8
+    assert np.linalg.norm(x - xo[:, 0]) <= tol * np.linalg.norm(xo)
+    # growth: no redraws -- every resketch keeps the sketch-0 seed, and m doubles
+    ms = [m for _, m in tr.schedule()]
+    assert ms == sorted(ms)
+
+
+def test_incremental_tf32_gaussian_converges():
+    """TF32 sketches perturb the decrements at the 1e-3 level, so the decision
+    times may differ from the fp64 oracle; the solve must still reach the
+    fp32 target and grow (not redraw) its sketch."""
+    import paper_2104_14101_b200 as ak
+
+    rng = np.random.default_rng(6)
+    n, d = 4096, 64
+    A = (rng.standard_normal((n, d)) / np.sqrt(n) * (1.0 / np.arange(1, d + 1))).astype(np.float32)
+    b = A.astype(np.float64).T @ (A.astype(np.float64) @ rng.standard_normal(d))
+    p = ak.RegularizedProblem(A, b, 0.01, dtype="float32")
+    sol = ak.direct_solve(p)
+    cfg = ak.AdaptiveConfig.for_method("ihs", 0.125, 8, 12, "gaussian", 1)
+    x, tr = ak.adaptive_run(p, np.zeros(d), cfg, method="ihs", incremental=True, tf32=True, sol=sol)
+    d0 = tr.records[0].delta_exact
+    assert tr.records[-1].delta_exact <= 1e-6 * d0
+    ms = [m for _, m in tr.schedule()]
+    assert ms == sorted(ms) and all(b == 2 * a for a, b in zip([8] + ms[:-1], ms))
