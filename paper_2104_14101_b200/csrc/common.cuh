@@ -90,6 +90,8 @@ enum WsSlot {
   WS_GEMV,       // partials of column GEMVs (precond apply)
   WS_GRAM,       // Gram / capacitance matrix being factored
   WS_APPLY,      // temporaries of the dense preconditioner apply
+  WS_SA0,        // native driver: the current sketch SA (referenced by the live preconditioner)
+  WS_SA1,        // native driver: the next sketch
   WS_COUNT
 };
 

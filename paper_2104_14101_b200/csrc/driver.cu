@@ -131,7 +131,11 @@ __global__ void k_rescale_rows(const T* __restrict__ src, int64_t n, double s, T
 
 struct Incremental {
   bool on = false;
-  DevBuf ybuf, pbuf;          // transforms of all blocks, draw orders
+  // transforms of all blocks and draw orders: stream-ordered pool blocks
+  // (not context workspaces) -- as large as A, released when the solve ends
+  DevBuf ybuf, pbuf;
+  void* y = nullptr;
+  void* perm = nullptr;
   std::vector<int64_t> npad;  // per block
   std::vector<size_t> yoff, poff;
   bool ready = false;
@@ -186,6 +190,8 @@ static int make_sketch_incr(adask_ctx* ctx, const adask_problem* pb, const adask
       }
       ADASK_TRY(inc.ybuf.alloc(ybytes, st));
       ADASK_TRY(inc.pbuf.alloc(pcount * sizeof(int64_t), st));
+      inc.y = inc.ybuf.p;
+      inc.perm = inc.pbuf.p;
       std::vector<int64_t> perm;
       size_t bi = 0;
       for (int64_t r0 = 0; r0 < pb->n; r0 += B, ++bi) {
@@ -194,17 +200,17 @@ static int make_sketch_incr(adask_ctx* ctx, const adask_problem* pb, const adask
         ADASK_TRY(gen_from_seed(blocked ? adask_derive_seed(seed0, (uint64_t)((cfg->row0 + r0) / B)) : seed0, &g));
         perm.assign((size_t)inc.npad[bi], 0);
         const void* Ab = (const char*)pb->A + (size_t)r0 * pb->lda * esz;
-        ADASK_TRY(srht_transform_impl(ctx, pb->dtype, Ab, rows, d, pb->lda, &g, (char*)inc.ybuf.p + inc.yoff[bi],
+        ADASK_TRY(srht_transform_impl(ctx, pb->dtype, Ab, rows, d, pb->lda, &g, (char*)inc.y + inc.yoff[bi],
                                       perm.data(), st));
-        ADASK_CUDA(cudaMemcpyAsync((int64_t*)inc.pbuf.p + inc.poff[bi], perm.data(), perm.size() * sizeof(int64_t),
+        ADASK_CUDA(cudaMemcpyAsync((int64_t*)inc.perm + inc.poff[bi], perm.data(), perm.size() * sizeof(int64_t),
                                    cudaMemcpyHostToDevice, st));
         ADASK_CUDA(cudaStreamSynchronize(st));  // perm (pageable host) is reused by the next block
       }
       inc.ready = true;
     }
     for (size_t bi = 0; bi < inc.npad.size(); ++bi)
-      ADASK_TRY(srht_gather_impl(ctx, pb->dtype, (char*)inc.ybuf.p + inc.yoff[bi], inc.npad[bi], d,
-                                 (const int64_t*)inc.pbuf.p + inc.poff[bi], m, SA, d, bi > 0 ? 1 : 0, st));
+      ADASK_TRY(srht_gather_impl(ctx, pb->dtype, (char*)inc.y + inc.yoff[bi], inc.npad[bi], d,
+                                 (const int64_t*)inc.perm + inc.poff[bi], m, SA, d, bi > 0 ? 1 : 0, st));
     if (pb->allreduce && pb->allreduce(SA, m * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
       return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
     return ADASK_OK;
@@ -280,8 +286,14 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
   };
 
   // sketch + build
-  DevBuf sa_buf;
-  ADASK_TRY(sa_buf.alloc((size_t)m * d * esz, st));
+  // SA buffers: two grow-only context workspaces (the live preconditioner
+  // references the current one; the next sketch goes to the other), so
+  // repeated solves allocate nothing once the largest sketch has been seen
+  struct SaBuf {
+    void* p = nullptr;
+  } sa_buf;
+  int sa_slot = WS_SA0;
+  ADASK_TRY(ctx->ws[sa_slot].get((size_t)m * d * esz, st, &sa_buf.p));
   Incremental inc;
   inc.on = (cfg->flags & ADASK_INCREMENTAL) != 0;
   if (inc.on)
@@ -341,13 +353,15 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
       capped_retry = at_cap;
       adask_precond_destroy(P);
       P = nullptr;
-      DevBuf nsa;
-      ADASK_TRY(nsa.alloc((size_t)m * d * esz, st));
+      const int nslot = sa_slot == WS_SA0 ? WS_SA1 : WS_SA0;
+      SaBuf nsa;
+      ADASK_TRY(ctx->ws[nslot].get((size_t)m * d * esz, st, &nsa.p));
       if (inc.on)
         ADASK_TRY(make_sketch_incr(ctx, pb, cfg, inc, m, sa_buf.p, m_old, nsa.p, st));
       else
         ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, (uint64_t)K), nsa.p, st));
-      std::swap(sa_buf.p, nsa.p);  // the previous SA is released (stream-ordered) with nsa
+      std::swap(sa_buf.p, nsa.p);
+      sa_slot = nslot;
       ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
                                     (void*)st));
       ADASK_TRY(restart());

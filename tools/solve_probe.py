@@ -18,7 +18,7 @@ p = ak.RegularizedProblem(A, b, cfg.nu, lam, validate=False)
 x0 = torch.zeros(cfg.d, dtype=torch.float64, device="cuda")
 acfg = ak.AdaptiveConfig.for_method(cfg.method, 0.125, cfg.m_init, T, cfg.family, 1)
 kw = {"tf32": cfg.dtype == "float32" and cfg.family == "gaussian", "block": cfg.block or (1 << 21)}
-for prof in (False, True, False):
+for prof in [False] * int(os.environ.get("ROUNDS", 1)) + [True, False]:
     dv.ctx().prof_enable(prof)
     for rep in range(3):
         torch.cuda.synchronize()
@@ -27,6 +27,12 @@ for prof in (False, True, False):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         print(f"prof={prof} rep={rep}: {dt*1e3:8.1f} ms  schedule={tr.schedule()}", flush=True)
+        if dt > 0.3:  # slow solve: where did the time go
+            last = 0.0
+            for r in tr.records:
+                if r.wall_seconds - last > 0.02:
+                    print(f"    slow step before record t={r.t} m={r.m} ev={r.event}: +{(r.wall_seconds-last)*1e3:.1f} ms")
+                last = r.wall_seconds
     if prof:
         q = dv.ctx().prof_query()
         print({k: (v['count'], round(v['ms'], 1)) for k, v in q.items() if v['count']})
