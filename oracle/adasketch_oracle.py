@@ -180,37 +180,6 @@ def philox_gaussian(m: int, n: int, seed: int, col0: int = 0) -> np.ndarray:
     return Z.reshape(4 * ngrp, n)[:m] / np.sqrt(m)
 
 
-def philox_gaussian_tf32(m: int, n: int, seed: int, col0: int = 0) -> np.ndarray:
-    """The TF32 tensor-core sketch's S (gauss_tc.cu, ADASK_TF32), restated:
-    for global column i and sketch-row octet g8 = k >> 3, Philox4x32-10 with
-    counter (i_lo, i_hi, g8, 0x54463332) and key = seed gives four words =
-    eight 16-bit halves h_0..h_7 (low half of word j is h_{2j});
-    u_t = (h_t + 1/2) 2^-16; (z_{2p}, z_{2p+1}) = sqrt(-2 ln u_{2p})
-    (cos, sin)(2 pi u_{2p+1}); S[k, i] = z_{k & 7} / sqrt(m)."""
-    key = (int(seed) & 0xFFFFFFFF, (int(seed) >> 32) & 0xFFFFFFFF)
-    ngrp = (m + 7) // 8
-    i = np.arange(col0, col0 + n, dtype=np.uint64)
-    g = np.arange(ngrp, dtype=np.uint64)
-    ctr = np.zeros((ngrp, n, 4), dtype=np.uint64)
-    ctr[..., 0] = (i & np.uint64(0xFFFFFFFF))[None, :]
-    ctr[..., 1] = (i >> np.uint64(32))[None, :]
-    ctr[..., 2] = g[:, None]
-    ctr[..., 3] = 0x54463332
-    o = philox4x32_10(ctr, key).astype(np.uint64)
-    h = np.empty((ngrp, n, 8), dtype=np.float64)
-    for j in range(4):
-        h[..., 2 * j] = (o[..., j] & np.uint64(0xFFFF)).astype(np.float64)
-        h[..., 2 * j + 1] = (o[..., j] >> np.uint64(16)).astype(np.float64)
-    u = (h + 0.5) * 2.0**-16
-    Z = np.empty((ngrp, 8, n))
-    for p in range(4):
-        rad = np.sqrt(-2.0 * np.log(u[..., 2 * p]))
-        th = 6.283185307179586 * u[..., 2 * p + 1]
-        Z[:, 2 * p] = rad * np.cos(th)
-        Z[:, 2 * p + 1] = rad * np.sin(th)
-    return Z.reshape(8 * ngrp, n)[:m] / np.sqrt(m)
-
-
 def sketch_gaussian(A: np.ndarray, m: int, seed: int, S: np.ndarray | None = None) -> np.ndarray:
     """embeddings.py:66-73 with the Philox S (or an injected S)."""
     A = np.asarray(A, dtype=np.float64)
@@ -454,15 +423,15 @@ class Trace:
 class IncrementalSketcher:
     """The library's incremental sketch growth (driver.cu: make_sketch_incr),
     restated: every sketch uses the seed of sketch 0 (derive_seed(seed, 0)).
-    Gaussian (Philox S, or the TF32 definition): the first sketch is S(m) A;
+    Gaussian (Philox S): the first sketch is S(m) A;
     growing to m' keeps the rows as SA * sqrt(m / m') and appends rows
     [m, m') of S(m') A.  SRHT / block SRHT: Y_b = fwht(D_b pad(A_b)) /
     sqrt(n_pad_b) once per block (signs = integers(0, 2, n_b) of the block's
     generator), perm_b = choice(n_pad_b, n_pad_b, replace=False) drawn next;
     SA(m) = sum_b Y_b[perm_b[:m]] * sqrt(n_pad_b / m)."""
 
-    def __init__(self, family: str, seed: int, block: int | None = None, tf32: bool = False):
-        self.family, self.seed0, self.block, self.tf32 = family, derive_seed(seed, 0), block, tf32
+    def __init__(self, family: str, seed: int, block: int | None = None):
+        self.family, self.seed0, self.block = family, derive_seed(seed, 0), block
         self.SA = None
         self.m = 0
         self.Y = None
@@ -470,7 +439,7 @@ class IncrementalSketcher:
     def __call__(self, A, m: int, _seed=None):
         A = np.asarray(A, dtype=np.float64)
         if self.family == "gaussian":
-            gen = philox_gaussian_tf32 if self.tf32 else philox_gaussian
+            gen = philox_gaussian
             if self.SA is None:
                 self.SA = gen(m, A.shape[0], self.seed0) @ A
             elif m != self.m:

@@ -37,8 +37,8 @@ extern "C" int adask_sketch_gaussian_rows(adask_ctx* ctx, int dtype, const void*
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
   const bool accumulate = (flags & ADASK_ACCUMULATE) != 0;
   ProfScope prof(ctx, PK_GAUSS, st, (double)n_local * d * esz, 2.0 * (double)mk * n_local * d);
-  // tcgen05 path needs 16-byte aligned rows (TMA) and an octet-aligned row offset; otherwise the FP32-pipe GEMM
-  if ((flags & ADASK_TF32) && dtype == ADASK_F32 && lda % 4 == 0 && ((uintptr_t)A & 15) == 0 && k0 % 8 == 0) {
+  // tcgen05 path needs 16-byte aligned rows (TMA) and a 4-aligned row offset; otherwise the FP32-pipe GEMM
+  if ((flags & ADASK_TF32) && dtype == ADASK_F32 && lda % 4 == 0 && ((uintptr_t)A & 15) == 0 && k0 % 4 == 0) {
     return gauss_tc_impl(ctx, (const float*)A, n_local, d, lda, row0, mk, key, (float*)SA, ldsa, accumulate, st,
                          k0, m_total);
   }

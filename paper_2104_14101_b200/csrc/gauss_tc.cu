@@ -6,8 +6,10 @@
 // tcgen05.mma.cta_group::2.kind::tf32 (M = 256, N = 256, K = 8, two MMAs per
 // K step), the accumulators in TMEM (each CTA: its 128 rows x 512 columns).
 // Per 32-row stage of A, each CTA's 16 generator warps write its 128 x 32
-// tile of S straight into shared memory in the MN-major SWIZZLE_128B_BASE32B
-// operand layout (one Philox call = eight sketch rows = one 32-byte chunk),
+// tile of S (the Gaussian entry definition of rng.cuh: gaussian_quad_f64,
+// evaluated in fast fp32) straight into shared memory in the MN-major
+// SWIZZLE_128B_BASE32B operand layout (one Philox call = four sketch rows =
+// one 16-byte chunk),
 // its TMA warp loads its half of the A tile (CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B),
 // and the even CTA's MMA thread issues the MMAs and commits to both CTAs'
 // ring barriers (4-stage ring, 48 KB per stage).  The epilogue warps drain
@@ -30,6 +32,7 @@ constexpr int BM = 128;  // sketch rows per CTA (TMEM lanes); a CTA pair covers 
 #endif
 constexpr int BK = ADASK_TC_BK;  // rows of A per pipeline stage
 constexpr int NGEN = 16;  // generator / epilogue warps (one stage row each per pass)
+constexpr int KQ = BK / NGEN;  // Philox calls per generator thread per stage
 constexpr int THREADS = 64 + 32 * NGEN;
 
 // Per CTA of the pair: NH MMAs of N = 256 per K step; this CTA holds 128 of
@@ -60,35 +63,21 @@ __device__ __forceinline__ float unit23(uint32_t w) {  // (w >> 9) * 2^-23, exac
   return __uint_as_float(0x3F800000u | (w >> 9)) - 1.0f;
 }
 
-// TF32 sketch entries (the product's definition for ADASK_TF32; the oracle's
-// philox_gaussian_tf32 restates it).  For global A row i and sketch-row octet
-// g8 = k >> 3: Philox4x32-10(counter = (i_lo, i_hi, g8, 0x54463332), key =
-// seed) gives four words = eight 16-bit halves h_0..h_7 (low half first);
-// u_t = (h_t + 1/2) 2^-16; (z_{2p}, z_{2p+1}) = sqrt(-2 ln u_{2p}) (cos, sin)
-// (2 pi u_{2p+1}); S[k, i] = z_{k & 7} / sqrt(m).  Sixteen-bit uniforms are
-// finer than the TF32 operand (10-bit mantissa) and halve the Philox work per
-// normal.  NQ octets are evaluated with interleaved rounds.
-constexpr uint32_t kTf32Tag = 0x54463332u;
-
-// 1 + (h + 1/2) 2^-16 for the 16-bit field of w at bit `pos`: one bit-field
-// insert into the float pattern 0x3F800040 (exact)
-__device__ __forceinline__ float one_plus_unit16(uint32_t w, uint32_t pos) {
-  uint32_t f, h;
-  asm("bfe.u32 %0, %1, %2, 16;" : "=r"(h) : "r"(w), "r"(pos));
-  asm("bfi.b32 %0, %1, %2, 7, 16;" : "=r"(f) : "r"(h), "r"(0x3F800040u));
-  return __uint_as_float(f);
-}
-
+// gaussian_quad_f64 (rng.cuh) in fast fp32 for NQ counters at once (the
+// rounds are interleaved so the NQ dependency chains overlap): Philox4x32-10
+// with precomputed round keys, Box-Muller on MUFU lg2 / sqrt / sin / cos.
+// cos(2 pi u) is evaluated as -cos(2 pi (u - 1/2)) to keep the MUFU argument
+// in [-pi, pi).
 template <int NQ>
-__device__ __forceinline__ void gaussian_octets_fast(const uint64_t* i, uint32_t g8, const uint32_t* rk0,
-                                                     const uint32_t* rk1, float4* out /* 2 NQ */) {
+__device__ __forceinline__ void gaussian_quads_fast(const uint64_t* i, uint32_t g, const uint32_t* rk0,
+                                                    const uint32_t* rk1, float4* out) {
   uint32_t x[NQ], y[NQ], z[NQ], w[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     x[q] = (uint32_t)i[q];
     y[q] = (uint32_t)(i[q] >> 32);
-    z[q] = g8;
-    w[q] = kTf32Tag;
+    z[q] = g;
+    w[q] = 0u;
   }
 #pragma unroll
   for (int r = 0; r < 10; ++r)
@@ -102,20 +91,12 @@ __device__ __forceinline__ void gaussian_octets_fast(const uint64_t* i, uint32_t
     }
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    const uint32_t o[4] = {x[q], y[q], z[q], w[q]};
-    float v[8];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const float ua = one_plus_unit16(o[p], 0) - 1.0f;           // u_{2p}
-      const float ub_c = one_plus_unit16(o[p], 16) - 1.5f;        // u_{2p+1} - 1/2
-      const float rad = sqrt_approx(-1.3862943611198906f * lg2_approx(ua));
-      float sn, cs;
-      __sincosf(6.2831853071795865f * ub_c, &sn, &cs);
-      v[2 * p] = -rad * cs;
-      v[2 * p + 1] = -rad * sn;
-    }
-    out[2 * q] = make_float4(v[0], v[1], v[2], v[3]);
-    out[2 * q + 1] = make_float4(v[4], v[5], v[6], v[7]);
+    const float ra = sqrt_approx(-1.3862943611198906f * lg2_approx(1.0f - unit23(x[q])));
+    const float rc = sqrt_approx(-1.3862943611198906f * lg2_approx(1.0f - unit23(z[q])));
+    float sa, ca, sc, cc;
+    __sincosf(6.2831853071795865f * (unit23(y[q]) - 0.5f), &sa, &ca);
+    __sincosf(6.2831853071795865f * (unit23(w[q]) - 0.5f), &sc, &cc);
+    out[q] = make_float4(-ra * ca, -ra * sa, -rc * cc, -rc * sc);
   }
 }
 
@@ -262,42 +243,45 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncwarp();
   } else {
     // ---------------------------------------------------------- S generators
-    // one Philox call per thread per stage: sketch rows 8 ro .. 8 ro + 7 of
-    // stage row kk = one 32-byte chunk of the MN-major operand
-    static_assert(BM * BK / 8 == 32 * NGEN, "one octet per generator thread per stage");
     const int gt = threadIdx.x - 64;  // 0 .. 32 NGEN - 1
-    const int ro = gt & 15;           // tile rows 8 ro .. 8 ro + 7
-    const int kk = gt >> 4;           // stage row
-    const uint32_t grp8 = (uint32_t)(((kg0 + m0) >> 3) + ro);  // global sketch-row octet
+    const int rg = gt & 31;           // tile rows 4rg .. 4rg+3
+    const int kk0 = gt >> 5;          // stage rows kk0 + NGEN q, q < KQ
+    const uint32_t grp = (uint32_t)(((kg0 + m0) >> 2) + rg);  // global sketch-row group
     uint32_t rk0[10], rk1[10];
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
       rk0[r] = key0 + (uint32_t)r * 0x9E3779B9u;
       rk1[r] = key1 + (uint32_t)r * 0xBB67AE85u;
     }
-    // MN-major SW128_BASE32B: MN group (ro >> 2) at BK*128 bytes, K row kk at
-    // 128 B, 32-byte chunk (ro & 3) XOR (kk & 3)
-    const uint32_t soff = (uint32_t)((ro >> 2) * (BK * 128) + kk * 128 + (((ro & 3) ^ (kk & 3)) << 5));
-    const uint64_t gi0 = (uint64_t)(row0 + kb + kk);
-    // GU stages per trip: GU independent Philox / Box-Muller chains
-    constexpr int GU = 2;
+    // MN-major SW128_BASE32B: MN group (rg >> 3) at BK*128 bytes, K row kk at
+    // 128 B, 32-byte chunk ((rg >> 1) & 3) XOR (kk & 3), 16-byte half rg & 1
+    const uint32_t soff = (uint32_t)((rg >> 3) * (BK * 128) + kk0 * 128 + ((((rg >> 1) & 3) ^ (kk0 & 3)) << 5) +
+                                     ((rg & 1) << 4));
+    const uint64_t gi0 = (uint64_t)(row0 + kb + kk0);
+    // GU stages per trip: GU x KQ independent Philox / Box-Muller chains
+    constexpr int GU = KQ >= 2 ? 1 : 2;
     for (int it0 = 0; it0 < nk; it0 += GU) {
-      float4 z[2 * GU];
-      uint64_t gi[GU];
+      float4 z[GU][KQ];
+      uint64_t gi[GU * KQ];
 #pragma unroll
-      for (int u = 0; u < GU; ++u) gi[u] = gi0 + (uint64_t)(it0 + u) * BK;
+      for (int u = 0; u < GU; ++u)
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) gi[u * KQ + q] = gi0 + (uint64_t)(it0 + u) * BK + NGEN * q;
       if (dbg & 4) {  // timing probe: no generation
 #pragma unroll
-        for (int u = 0; u < 2 * GU; ++u) z[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < GU; ++u)
+#pragma unroll
+          for (int q = 0; q < KQ; ++q) z[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
       } else if (dbg == 1) {  // S[r, k] = [r == k mod 128] (layout debugging)
 #pragma unroll
-        for (int u = 0; u < GU; ++u) {
-          const int kl = (int)((gi[u] - (uint64_t)row0) & 127), r0 = 8 * ro;
-          z[2 * u] = make_float4(r0 == kl, r0 + 1 == kl, r0 + 2 == kl, r0 + 3 == kl);
-          z[2 * u + 1] = make_float4(r0 + 4 == kl, r0 + 5 == kl, r0 + 6 == kl, r0 + 7 == kl);
-        }
+        for (int u = 0; u < GU; ++u)
+#pragma unroll
+          for (int q = 0; q < KQ; ++q) {
+            const int kl = (int)((gi[u * KQ + q] - (uint64_t)row0) & 127);
+            z[u][q] = make_float4(4 * rg == kl, 4 * rg + 1 == kl, 4 * rg + 2 == kl, 4 * rg + 3 == kl);
+          }
       } else {
-        gaussian_octets_fast<GU>(gi, grp8, rk0, rk1, z);
+        gaussian_quads_fast<GU * KQ>(gi, grp, rk0, rk1, &z[0][0]);
       }
 #pragma unroll
       for (int u = 0; u < GU; ++u) {
@@ -309,9 +293,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         wait_or_trap(&empty[s], ph ^ 1u, 3);
         if (trace) tr0 += clock64() - tw;
         const uint32_t sdst = smem_u32(smem + s * C::STAGE_BYTES) + soff;
-        st_shared_v4(sdst, z[2 * u]);
-        st_shared_v4(sdst + 16, z[2 * u + 1]);
-        if (!(dbg & 64)) umma::fence_proxy_async_smem();
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) st_shared_v4(sdst + NGEN * 128 * q, z[u][q]);
+        umma::fence_proxy_async_smem();
         const long long tb = trace ? clock64() : 0;
         named_bar_sync(1, 32 * NGEN);
         if (trace) tr1 += clock64() - tb;
@@ -411,11 +395,11 @@ int launch_tc(adask_ctx* ctx, const CUtensorMap& map, int64_t n_local, int64_t d
 
 }  // namespace
 
-// Rows [kg0, kg0 + m) of the m_total-row TF32 sketch (kg0 a multiple of 8).
+// Rows [kg0, kg0 + m) of the m_total-row sketch (kg0 a multiple of 4).
 int gauss_tc_impl(adask_ctx* ctx, const float* A, int64_t n_local, int64_t d, int64_t lda, int64_t row0,
                   int64_t m, uint64_t key, float* SA, int64_t ldsa, bool accumulate, cudaStream_t st, int64_t kg0,
                   int64_t m_total) {
-  if (kg0 % 8 != 0) return fail(ADASK_E_ARG, "TF32 Gaussian sketch: row offset must be a multiple of 8");
+  if (kg0 % 4 != 0) return fail(ADASK_E_ARG, "TF32 Gaussian sketch: row offset must be a multiple of 4");
   if (n_local == 0) {
     if (!accumulate) ADASK_CUDA(cudaMemset2DAsync(SA, ldsa * 4, 0, d * 4, m, st));
     return ADASK_OK;

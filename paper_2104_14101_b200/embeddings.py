@@ -123,6 +123,21 @@ def gaussian_dev(Ad: torch.Tensor, m: int, seed: int, *, row0: int = 0, tf32: bo
     return SA
 
 
+def gaussian_rows_dev(Ad: torch.Tensor, m_total: int, k0: int, mk: int, seed: int, *, row0: int = 0,
+                      tf32: bool = False) -> torch.Tensor:
+    """Rows [k0, k0 + mk) of the m_total-row Gaussian sketch (entries scaled by
+    1/sqrt(m_total)): the building block of incremental sketch growth."""
+    n, d = Ad.shape
+    SA = torch.empty((int(mk), d), dtype=Ad.dtype, device=Ad.device)
+    _lib.check(
+        _lib.lib().adask_sketch_gaussian_rows(dv.ctx().handle, dv.dtype_code(Ad.dtype), Ad.data_ptr(), n, d,
+                                              Ad.stride(0), int(row0), int(m_total), int(k0), int(mk),
+                                              int(seed) & 0xFFFFFFFFFFFFFFFF, SA.data_ptr(), SA.stride(0),
+                                              _lib.TF32 if tf32 else 0, dv.stream()),
+        "sketch_gaussian_rows")
+    return SA
+
+
 def srht_dev(Ad: torch.Tensor, m: int, seed: int, *, out: torch.Tensor | None = None,
              accumulate: bool = False, return_idx: bool = False):
     n, d = Ad.shape

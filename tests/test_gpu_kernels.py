@@ -186,9 +186,7 @@ def _tf32_case(n, d, m, row0, seed, accumulate=False):
     rng = np.random.default_rng(n + d + m)
     A = rng.standard_normal((n, d)).astype(np.float32)
     Ad = torch.from_numpy(A).cuda()
-    # the TF32 path has its own entry definition (16-bit uniforms); the FP32-pipe
-    # fallback (rows not 16-byte aligned) keeps the fp64 / fp32 definition
-    S = (O.philox_gaussian_tf32 if d % 4 == 0 else O.philox_gaussian)(m, n, seed, col0=row0)
+    S = O.philox_gaussian(m, n, seed, col0=row0)
     ref = S @ A.astype(np.float64)
     bound = np.abs(S) @ np.abs(A.astype(np.float64))
     base = None
@@ -227,3 +225,23 @@ def test_gaussian_tf32_accumulate_and_shards():
     part = gaussian_dev(A[:2048], 96, 3, tf32=True)
     part = gaussian_dev(A[2048:], 96, 3, row0=2048, tf32=True, out=part, accumulate=True)
     torch.testing.assert_close(part, whole, rtol=0, atol=2e-5)
+
+
+@pytest.mark.parametrize("k0,mk,m_total,dtype,tf32", [(0, 64, 64, "float64", False), (64, 64, 128, "float64", False),
+                                                      (13, 50, 200, "float64", False), (256, 256, 512, "float32", True),
+                                                      (6, 30, 64, "float32", True)])
+def test_gaussian_rows_offset_matches_oracle(k0, mk, m_total, dtype, tf32):
+    from paper_2104_14101_b200.embeddings import gaussian_rows_dev
+
+    rng = np.random.default_rng(k0 + mk)
+    n, d = 2000, 96
+    A = rng.standard_normal((n, d))
+    Ad = torch.from_numpy(A).to("cuda", torch.float32 if dtype == "float32" else torch.float64)
+    got = gaussian_rows_dev(Ad, m_total, k0, mk, 11, row0=3, tf32=tf32).double().cpu().numpy()
+    S = O.philox_gaussian(m_total, n, 11, col0=3)[k0:k0 + mk]
+    Aref = Ad.double().cpu().numpy()
+    ref = S @ Aref
+    if dtype == "float64":
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    else:
+        assert np.all(np.abs(got - ref) <= 2.0**-9 * (np.abs(S) @ np.abs(Aref)) + 1e-5)
