@@ -72,20 +72,23 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
+    def _sample(self, busy_only: bool):
+        try:
+            mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+            util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            if util > 0 or not busy_only:
+                self.samples.append(mhz)
+            for bit, name in self.REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
-                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                if util > 0:
-                    self.samples.append(mhz)
-                for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.05)
+            self._sample(busy_only=True)
+            time.sleep(0.01)
 
     def __enter__(self):
         if self.nv:
@@ -97,6 +100,8 @@ class ClockSampler:
         self._stop.set()
         if self.nv:
             self.t.join()
+            if not self.samples:  # a timed region shorter than the sampling period
+                self._sample(busy_only=False)
 
     def summary(self) -> dict:
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
