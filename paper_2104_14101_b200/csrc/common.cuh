@@ -92,6 +92,7 @@ enum WsSlot {
   WS_APPLY,      // temporaries of the dense preconditioner apply
   WS_SA0,        // native driver: the current sketch SA (referenced by the live preconditioner)
   WS_SA1,        // native driver: the next sketch
+  WS_SRHT_U,     // pipelined SRHT: the two half transforms of an 11-bit pass 2
   WS_COUNT
 };
 

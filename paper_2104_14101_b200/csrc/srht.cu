@@ -295,6 +295,9 @@ static int fwht_select(adask_ctx* ctx, int dtype, const void* A, int64_t n, int6
                        const uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m,
                        void* out, int64_t ldo, double c1, double c2, int accumulate,
                        cudaStream_t st) {
+  // 2^12..2^22 padded rows: persistent TMA-pipelined passes (srht_pipe.cu)
+  if (fwht_pipe_eligible(dtype, A, n, n_pad, lda, m, idx != nullptr))
+    return fwht_select_pipe(ctx, dtype, A, n, d, lda, sgn, n_pad, idx, m, out, ldo, c1, c2, accumulate, st);
   const int L = ilog2(n_pad);
   int b1 = std::max(std::min(L, 10), L - 12);
   // many slots (m >= 4096 of >= 2^20 rows): the 11-bit pass-1 tiles and the
@@ -404,7 +407,7 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4));
   // signs: draws [0, n) of integers(0, 2)
   void* sw = nullptr;
-  ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(n, 32) * 4 + 16, st, &sw));
+  ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(1ll << ilog2(n), 32) * 4 + 64, st, &sw));  // padded: bulk-copied per tile
   uint32_t* sgn = (uint32_t*)sw;
   ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
   // idx = choice(n_pad, m, replace=False) after the n sign draws (host)
@@ -433,7 +436,7 @@ int srht_transform_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int
   if (ilog2(n_pad) > 24) return fail(ADASK_E_ARG, "srht_transform: n_pad > 2^24 unsupported");
   ProfScope prof(ctx, PK_SRHT, st, (double)(n + n_pad) * d * (dtype == ADASK_F64 ? 8 : 4));
   void* sw = nullptr;
-  ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(n, 32) * 4 + 16, st, &sw));
+  ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(1ll << ilog2(n), 32) * 4 + 64, st, &sw));  // padded: bulk-copied per tile
   uint32_t* sgn = (uint32_t*)sw;
   ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
   if (perm_host) {

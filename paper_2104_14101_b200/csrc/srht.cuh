@@ -12,4 +12,10 @@ int srht_transform_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int
                         const adask_pcg64* g, void* Y, int64_t* perm_host, cudaStream_t st);
 int srht_gather_impl(adask_ctx* ctx, int dtype, const void* Y, int64_t n_pad, int64_t d, const int64_t* perm_dev,
                      int64_t m, void* SA, int64_t ldsa, int accumulate, cudaStream_t st);
+// Pipelined pruned FWHT (srht_pipe.cu): persistent TMA-fed tile passes.
+int fwht_pipe_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int64_t lda, int64_t m, bool selected);
+int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                     const uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out, int64_t ldo,
+                     double c1, double c2, int accumulate, cudaStream_t st);
+int fwht_build_map2(adask_ctx* ctx, const int32_t* pos, int64_t m, int32_t* map2, int64_t rows, cudaStream_t st);
 }  // namespace adask

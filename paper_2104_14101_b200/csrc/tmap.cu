@@ -58,4 +58,22 @@ int tensor_map_2d(CUtensorMap* map, int dtype, const void* base, int64_t rows, i
   return ADASK_OK;
 }
 
+int tensor_map_rows3d(CUtensorMap* map, int dtype, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                      uint32_t box_cols, uint32_t box_q, uint32_t e) {
+  int st = ADASK_OK;
+  auto encode = encoder(&st);
+  if (!encode) return st;
+  if (rows % e) return fail(ADASK_E_ARG, "tensor_map_rows3d: %lld rows not a multiple of %u", (long long)rows, e);
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)(rows / e), (cuuint64_t)e};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * esz * e, (cuuint64_t)ld * esz};
+  cuuint32_t box[3] = {box_cols, box_q, e};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, dtype == ADASK_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                      (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ADASK_E_CUDA, "cuTensorMapEncodeTiled (3-D rows) failed (%d)", (int)r);
+  return ADASK_OK;
+}
+
 }  // namespace adask

@@ -200,5 +200,10 @@ int tensor_map_f32_sw128(CUtensorMap* map, const float* base, int64_t rows, int6
 // Plain (unswizzled) 2-D row-major tensor map of fp64 / fp32 (dtype ADASK_F64 / F32).
 int tensor_map_2d(CUtensorMap* map, int dtype, const void* base, int64_t rows, int64_t cols, int64_t ld,
                   uint32_t box_cols, uint32_t box_rows);
+// Rows of a row-major matrix viewed as {cols, rows / e, e} with strides
+// {1, e*ld, ld} elements (rows must be a multiple of e): a box
+// {box_cols, box_q, e} lands in shared memory as [e][q][col].
+int tensor_map_rows3d(CUtensorMap* map, int dtype, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                      uint32_t box_cols, uint32_t box_q, uint32_t e);
 
 }  // namespace adask

@@ -114,6 +114,37 @@ def test_srht_bitwise(ak, n, d, m, seed):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("n,d,m,seed", [(4096, 24, 40, 1), (1 << 14, 20, 1 << 14, 2), (65536, 40, 4096, 3),
+                                        ((1 << 16) + 32, 17, 513, 4), (1 << 20, 6, 2000, 5), (1 << 21, 3, 3000, 6)])
+def test_srht_pipelined_passes_bitwise(ak, n, d, m, seed, monkeypatch):
+    """The persistent TMA-pipelined FWHT passes (srht_pipe.cu, forced with
+    ADASK_FWHT_PIPE=2) reproduce the reference SRHT bit for bit (fp64),
+    including the 10-bit-per-half pass 2 plus last-stage combine at 2^21 rows."""
+    monkeypatch.setenv("ADASK_FWHT_PIPE", "2")
+    A = np.random.default_rng(seed).standard_normal((n, d))
+    got = ak.sketch_srht(A, m, seed).SA
+    assert np.array_equal(got, O.sketch_srht(A, m, seed))
+
+
+@pytest.mark.parametrize("n,d,m", [(1 << 16, 64, 64), (1 << 16, 48, 4096), ((1 << 21) - 64, 16, 32768),
+                                   (1 << 21, 20, 100)])
+def test_srht_pipelined_fp32_matches_tile_kernels(ak, n, d, m, monkeypatch):
+    """fp32 data: the pipelined passes run the same butterfly DAG as the tile
+    kernels, so the two device paths agree bitwise; both are within fp32
+    rounding of the fp64 oracle."""
+    from paper_2104_14101_b200.embeddings import srht_dev
+
+    A = torch.randn(n, d, dtype=torch.float32, device="cuda", generator=torch.Generator("cuda").manual_seed(n + m))
+    monkeypatch.setenv("ADASK_FWHT_PIPE", "2")
+    pipe = srht_dev(A, m, 9)
+    monkeypatch.setenv("ADASK_FWHT_PIPE", "0")
+    tile = srht_dev(A, m, 9)
+    assert torch.equal(pipe, tile)
+    if n <= 1 << 16:
+        ref = O.sketch_srht(A.double().cpu().numpy(), m, 9)
+        assert np.linalg.norm(pipe.double().cpu().numpy() - ref) <= 1e-5 * np.linalg.norm(ref)
+
+
 @pytest.mark.parametrize("n,d", [(1, 1), (8, 3), (1024, 5), (4096, 2), (1 << 15, 3)])
 def test_fwht_bitwise(ak, n, d):
     x = np.random.default_rng(n).standard_normal((n, d))
