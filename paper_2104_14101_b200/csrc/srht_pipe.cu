@@ -231,6 +231,37 @@ __device__ __forceinline__ void pipe_round(typename Lane8<T>::V* scr, int tid) {
   }
 }
 
+// Last pass-1 round with every slot needed: the butterflies' results go from
+// registers straight to Z (8-byte lanes, 64-byte row segments per 8 lanes),
+// skipping the scratch write-back and the copy-out pass.
+template <typename T, int BT, int W8, int NB, int NB0, int LO, int NT>
+__device__ __forceinline__ void pipe_round_emit(const typename Lane8<T>::V* scr, int tid, T* zb, int64_t sstride,
+                                                int64_t col0, int64_t d) {
+  using V = typename Lane8<T>::V;
+  constexpr int E = 1 << NB;
+  constexpr int UNITS = BT * W8 / E;
+  constexpr int HI = LO + NB;
+  constexpr int CPL = 8 / (int)sizeof(T);  // columns per 8-byte lane
+  static_assert(UNITS % NT == 0, "emit units");
+#pragma unroll 1
+  for (int u = tid; u < UNITS; u += NT) {
+    const int c = u % W8, q = u / W8;
+    int P[4];
+    const int base = prow(q, 0, LO, HI);
+    unit_bases<NB0, LO, E>(base, P);
+    V v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = scr[(P[e & 3] + ((e >> 2) << (LO + 2))) * W8 + c];
+    butterflies_x<T, NB, 0>(v, 0);
+    if (col0 + c * CPL < d) {
+      T* z = zb + (int64_t)base * sstride + c * CPL;
+      const int64_t step = sstride << LO;
+#pragma unroll
+      for (int e = 0; e < E; ++e) *reinterpret_cast<V*>(z + e * step) = v[e];
+    }
+  }
+}
+
 template <typename T, int LOG, int LOGT, int SEGB, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_fwht_pipe(const __grid_constant__ CUtensorMap smap, PipeArgs a) {
   using S = PipeShape<LOG, LOGT, SEGB, T, MODE>;
@@ -363,12 +394,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwht_pipe(const __grid_constant
       named_bar_sync(1, NT);
       pipe_round<T, BT, W8, 5, NB0, 5, NT>(scr, tid);
     }
+    // pass 1 with every slot needed (m >= 2^10 rows selected): direct emit
+    const bool direct = MODE == P1 && S::ROUNDS == 2 && a.nslots == (1 << LOG);
     if constexpr (S::ROUNDS > 1) {
       constexpr int LO = 5 * (S::ROUNDS - 1);
       named_bar_sync(1, NT);
-      pipe_round<T, BT, W8, LOG - LO, NB0, LO, NT>(scr, tid);
+      if (direct)
+        pipe_round_emit<T, BT, W8, LOG - LO, NB0, LO, NT>(scr, tid, reinterpret_cast<T*>(a.Z) + ti * a.ldz + col0,
+                                                         a.G * a.ldz, col0, a.d);
+      else
+        pipe_round<T, BT, W8, LOG - LO, NB0, LO, NT>(scr, tid);
     }
     TR_MARK(t1c);
+    if (direct) continue;
     named_bar_sync(1, NT);
     TR_MARK(tb);
 
@@ -621,6 +659,12 @@ int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
     for (int64_t k = 0; k < m; ++k) lo2slot[(size_t)(idx[k] & (B - 1))] = 0;
     for (int64_t lo = 0; lo < B; ++lo)
       if (lo2slot[(size_t)lo] == 0) lo2slot[(size_t)lo] = (int32_t)nslots++;
+    // nearly every slot needed: keep all of them (identity slots) so that
+    // pass 1 emits Z straight from registers (the few unused rows are free)
+    if (nslots * 16 >= B * 15) {
+      for (int64_t lo = 0; lo < B; ++lo) lo2slot[(size_t)lo] = (int32_t)lo;
+      nslots = B;
+    }
     plan.resize((size_t)(B + m));
     std::copy(lo2slot.begin(), lo2slot.end(), plan.begin());
     for (int64_t k = 0; k < m; ++k)

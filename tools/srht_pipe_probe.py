@@ -10,7 +10,7 @@ from paper_2104_14101_b200.embeddings import srht_dev
 
 
 def run(A, m, seed, pipe):
-    os.environ["ADASK_FWHT_PIPE"] = "1" if pipe else "0"
+    os.environ["ADASK_FWHT_PIPE"] = "2" if pipe else "0"
     return srht_dev(A, m, seed)
 
 
