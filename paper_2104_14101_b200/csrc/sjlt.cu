@@ -123,6 +123,12 @@ static int launch_accumulate(adask_ctx* ctx, const T* A, int64_t d, int64_t lda,
                              const int32_t* order, const int32_t* start, const int32_t* sgn,
                              int32_t s, int64_t m, T* SA, int64_t ldsa, int accumulate,
                              cudaStream_t st) {
+  {
+    int launched = 0;
+    ADASK_TRY(sjlt_accumulate_pipe(ctx, sizeof(T) == 8 ? ADASK_F64 : ADASK_F32, A, d, lda, order, start, sgn, s, m,
+                                   SA, ldsa, accumulate, st, &launched));
+    if (launched) return ADASK_OK;
+  }
   constexpr int VEC = 16 / sizeof(T);
   const bool aligned = ((uintptr_t)A % 16 == 0) && ((lda * (int64_t)sizeof(T)) % 16 == 0);
   const int threads = 128;

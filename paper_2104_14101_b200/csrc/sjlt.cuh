@@ -8,4 +8,9 @@ int sketch_sjlt_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n_local, 
                      void* SA, int64_t ldsa, uint32_t flags, cudaStream_t st);
 int bucket_sort(adask_ctx* ctx, const int32_t* keys, int64_t nent, int64_t m, int32_t s,
                 const int32_t** order_out, const int32_t** start_out, cudaStream_t st);
+// Bulk-copy streamed bucket accumulation (sjlt_pipe.cu); *launched = 0 when
+// the shape is not eligible (then the caller uses its own kernel).
+int sjlt_accumulate_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t d, int64_t lda, const int32_t* order,
+                         const int32_t* start, const int32_t* sgn, int32_t s, int64_t m, void* SA, int64_t ldsa,
+                         int accumulate, cudaStream_t st, int* launched);
 }  // namespace adask

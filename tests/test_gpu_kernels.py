@@ -145,6 +145,21 @@ def test_srht_pipelined_fp32_matches_tile_kernels(ak, n, d, m, monkeypatch):
         assert np.linalg.norm(pipe.double().cpu().numpy() - ref) <= 1e-5 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("n,d,m,s", [(5000, 34, 300, 1), (70000, 2048, 512, 1), (9000, 64, 4096, 1),
+                                     (3000, 48, 40, 3), (20000, 96, 700, 2)])
+def test_sjlt_streamed_accumulation_bitwise(ak, n, d, m, s, monkeypatch):
+    """The bulk-copy streamed bucket accumulation (sjlt_pipe.cu, forced with
+    ADASK_SJLT_PIPE=2) equals the reference's csr product bit for bit."""
+    monkeypatch.setenv("ADASK_SJLT_PIPE", "2")
+    A = np.random.default_rng(n + m).standard_normal((n, d))
+    got = ak.sketch_sjlt(A, m, 17, s=s).SA
+    ref = O.sketch_sjlt(A, m, 17, s=s)
+    if s == 1:
+        assert np.array_equal(got, ref)
+    else:
+        np.testing.assert_allclose(got, ref, rtol=1e-15, atol=1e-15)
+
+
 @pytest.mark.parametrize("n,d", [(1, 1), (8, 3), (1024, 5), (4096, 2), (1 << 15, 3)])
 def test_fwht_bitwise(ak, n, d):
     x = np.random.default_rng(n).standard_normal((n, d))
