@@ -10,11 +10,17 @@ namespace adask {
 
 // out[i] = alpha * sum_{j in J(i)} M[i*ld + j] * x[j]   (+ beta_vec? handled by caller)
 // mode 0: J = [0, cols), 1: J = [0, i] (lower), 2: J = [i, cols) (upper)
+// One warp per row.  The matrix is small and L2-resident (explicit factor
+// inverses, SA), so each warp issues up to 8 x 16-byte loads per lane before
+// the first FMA: a 1024-wide fp64 row is two load rounds, not eight
+// dependent ones (the load latency, not bandwidth, bounds this kernel).
 template <typename T>
 __global__ void __launch_bounds__(256) k_gemv_rows(const T* __restrict__ M, int64_t rows,
                                                    int64_t cols, int64_t ld,
                                                    const double* __restrict__ x, double alpha,
-                                                   double* __restrict__ out, int mode) {
+                                                   double* __restrict__ out, int mode, int vec) {
+  constexpr int CE = 16 / (int)sizeof(T);  // elements per 16-byte chunk
+  constexpr int U = 8;
   const int lane = threadIdx.x & 31;
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= rows) return;
@@ -22,18 +28,54 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const T* __restrict__ M, int6
   if (mode == 1) j1 = i + 1 < cols ? i + 1 : cols;
   if (mode == 2) j0 = i;
   const T* r = M + i * ld;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int64_t j = j0 + lane;
-  for (; j + 96 < j1; j += 128) {
-    s0 = fma((double)r[j], x[j], s0);
-    s1 = fma((double)r[j + 32], x[j + 32], s1);
-    s2 = fma((double)r[j + 64], x[j + 64], s2);
-    s3 = fma((double)r[j + 96], x[j + 96], s3);
+  double s[CE];
+#pragma unroll
+  for (int v = 0; v < CE; ++v) s[v] = 0.0;
+  if (vec) {
+    // 16-byte chunks [c0, c1) covering [j0, j1); elements outside are masked
+    const int64_t c0 = j0 / CE, c1 = (j1 + CE - 1) / CE;
+    for (int64_t cb = c0 + lane; cb < c1; cb += 32 * U) {
+      T a[U][CE];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = cb + 32 * u;
+        if (c < c1) {
+          if constexpr (sizeof(T) == 8) {
+            const double2 q = __ldg(reinterpret_cast<const double2*>(r) + c);
+            a[u][0] = q.x;
+            a[u][1 % CE] = q.y;
+          } else {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(r) + c);
+            a[u][0] = q.x;
+            a[u][1 % CE] = q.y;
+            a[u][2 % CE] = q.z;
+            a[u][3 % CE] = q.w;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < CE; ++v) a[u][v] = (T)0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = cb + 32 * u;
+        if (c < c1) {
+#pragma unroll
+          for (int v = 0; v < CE; ++v) {
+            const int64_t j = c * CE + v;
+            if (j >= j0 && j < j1) s[v] = fma((double)a[u][v], x[j], s[v]);
+          }
+        }
+      }
+    }
+  } else {
+    for (int64_t j = j0 + lane; j < j1; j += 32) s[0] = fma((double)r[j], x[j], s[0]);
   }
-  for (; j < j1; j += 32) s0 = fma((double)r[j], x[j], s0);
-  double s = (s0 + s1) + (s2 + s3);
-  s = warp_sum(s);
-  if (lane == 0) out[i] = alpha * s;
+  double t = s[0];
+#pragma unroll
+  for (int v = 1; v < CE; ++v) t += s[v];
+  t = warp_sum(t);
+  if (lane == 0) out[i] = alpha * t;
 }
 
 // part[b][j] = sum_{i in rows of chunk b} M[i*ld + j] * u[i]
@@ -45,7 +87,15 @@ __global__ void k_gemv_cols(const T* __restrict__ M, int64_t rows, int64_t cols,
   const int64_t r0 = rows * blockIdx.y / nb, r1 = rows * (blockIdx.y + 1) / nb;
   if (j >= cols) return;
   double s = 0.0;
-  for (int64_t i = r0; i < r1; ++i) s = fma(u[i], (double)M[i * ld + j], s);
+  int64_t i = r0;
+  for (; i + 8 <= r1; i += 8) {  // eight loads in flight, then the FMAs in row order
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = (double)M[(i + q) * ld + j];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = fma(u[i + q], a[q], s);
+  }
+  for (; i < r1; ++i) s = fma(u[i], (double)M[i * ld + j], s);
   part[(int64_t)blockIdx.y * cols + j] = s;
 }
 
@@ -70,10 +120,12 @@ int gemv_rows(adask_ctx* ctx, int dtype, const void* M, int64_t rows, int64_t co
               const double* x, double alpha, double* out, int mode, cudaStream_t st) {
   if (rows <= 0) return ADASK_OK;
   const unsigned blocks = (unsigned)cdiv(rows * 32, 256);
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  const int vec = ((uintptr_t)M % 16 == 0) && ((size_t)ld * esz) % 16 == 0;
   if (dtype == ADASK_F64)
-    k_gemv_rows<double><<<blocks, 256, 0, st>>>((const double*)M, rows, cols, ld, x, alpha, out, mode);
+    k_gemv_rows<double><<<blocks, 256, 0, st>>>((const double*)M, rows, cols, ld, x, alpha, out, mode, vec);
   else
-    k_gemv_rows<float><<<blocks, 256, 0, st>>>((const float*)M, rows, cols, ld, x, alpha, out, mode);
+    k_gemv_rows<float><<<blocks, 256, 0, st>>>((const float*)M, rows, cols, ld, x, alpha, out, mode, vec);
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;
 }

@@ -25,6 +25,15 @@
 namespace adask {
 int problem_hess(adask_ctx* ctx, const adask_problem* pb, const double* X, const double* B, double* out,
                  cudaStream_t st);
+int pcg_propose_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P, const double* x,
+                     const double* r, const double* p, const double* dt_col, double* Hp, double* x_new,
+                     double* r_new, double* rt_new, double* dt_new, double* delta_tilde_host, double* hx_mb,
+                     int* hx_ok, cudaStream_t st);
+int pcg_restart_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P, const double* x,
+                     double* r, double* rt, double* p, double* dt_col, double* delta_tilde_host,
+                     const double* hx_mb, cudaStream_t st);
+int ihs_restart_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P, const double* x, double* g,
+                     double* v, double* delta_tilde_host, bool have_g, cudaStream_t st);
 
 __global__ void k_sub(int64_t n, const double* a, const double* b, double* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -248,12 +257,13 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
   *n_recs = 0;
   // state buffers
   DevBuf vecs;
-  ADASK_TRY(vecs.alloc((size_t)(12 * cd + 4 * c) * sizeof(double), st));
+  ADASK_TRY(vecs.alloc((size_t)(13 * cd + 4 * c) * sizeof(double), st));
   double* base = (double*)vecs.p;
   double *x = base, *xn = base + cd, *a1 = base + 2 * cd, *a2 = base + 3 * cd, *a3 = base + 4 * cd;
   double *b1 = base + 5 * cd, *b2 = base + 6 * cd, *b3 = base + 7 * cd, *xp = base + 8 * cd;
   double *diff = base + 9 * cd, *Hd = base + 10 * cd, *Hp = base + 11 * cd;
   double *dtc = base + 12 * cd, *dtn = dtc + c;  // per-column r.rt (current / proposed)
+  double* hxc = dtn + c;  // PCG: H x - B at the current iterate, from the proposal's fused pass
   ADASK_CUDA(cudaMemcpyAsync(x, x0, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
 
   const int64_t n_pad_total = (int64_t)1 << (int)std::ceil(std::log2((double)std::max<int64_t>(cfg->n_total, 1)));
@@ -321,9 +331,16 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
   }
   // PCG: a1 = r, a2 = rt, a3 = p ; b1 = r_new, b2 = rt_new ; IHS: a1 = g, a2 = v, b1 = g_new, b2 = v_new
   double delta = 0.0;
+  // Restarts after a resketch reuse H x - B at the unchanged iterate: IHS from
+  // its gradient buffer, PCG from the proposal's two-column pass (hx_ok).
+  // Both are the values the reference's recomputation gives, bit for bit.
+  int hx_ok = 0;
+  bool g_ok = false;
+  const bool reuse = getenv("ADASK_NO_RESTART_REUSE") == nullptr;
   auto restart = [&]() -> int {
-    if (pcg) return adask_pcg_restart(ctx, pb, P, x, a1, a2, a3, dtc, &delta, (void*)st);
-    ADASK_TRY(adask_ihs_restart(ctx, pb, P, x, a1, a2, &delta, (void*)st));
+    if (pcg) return pcg_restart_impl(ctx, pb, P, x, a1, a2, a3, dtc, &delta, reuse && hx_ok ? hxc : nullptr, st);
+    ADASK_TRY(ihs_restart_impl(ctx, pb, P, x, a1, a2, &delta, reuse && g_ok, st));
+    g_ok = true;
     if (polyak) ADASK_CUDA(cudaMemcpyAsync(xp, x, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
     return ADASK_OK;
   };
@@ -336,7 +353,8 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
   while (t < cfg->T) {
     double dnew = 0.0;
     if (pcg)
-      ADASK_TRY(adask_pcg_propose(ctx, pb, P, x, a1, a3, dtc, Hp, xn, b1, b2, dtn, &dnew, (void*)st));
+      ADASK_TRY(pcg_propose_impl(ctx, pb, P, x, a1, a3, dtc, Hp, xn, b1, b2, dtn, &dnew, reuse ? hxc : nullptr,
+                                 &hx_ok, st));
     else
       ADASK_TRY(adask_ihs_propose(ctx, pb, P, x, a2, mu, polyak ? xp : nullptr, beta, xn, b1, b2, &dnew,
                                   (void*)st));

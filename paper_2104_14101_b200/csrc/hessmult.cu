@@ -149,10 +149,14 @@ __global__ void __launch_bounds__(256) k_hess_fused(const T* __restrict__ A, int
 // 16-byte column chunks from SMEM, release the stage, reduce the R row dots
 // across the CTA (one named barrier per stage) and accumulate y_r a_r in
 // registers.  Bytes in flight no longer depend on occupancy or registers.
-template <typename T, int NCH, int R, int STAGES>
+template <typename T, int NCH, int R, int STAGES, int NX>
 __global__ void __launch_bounds__(288, 1) k_hess_tma(const T* __restrict__ A, int64_t n, int64_t d,
-                                                     int64_t lda, const double* __restrict__ x,
-                                                     double* __restrict__ part) {
+                                                     int64_t lda, const double* __restrict__ x0,
+                                                     const double* __restrict__ x1, double* __restrict__ part0,
+                                                     double* __restrict__ part1) {
+  // NX = 2: the same pass over A serves two right-hand sides (the PCG
+  // proposal direction and the current iterate); every column's arithmetic
+  // is the NX = 1 sequence, so each result is bitwise the single-column one
   constexpr int V = 16 / sizeof(T);
   constexpr int NW = 8;  // consumer warps
   extern __shared__ __align__(128) unsigned char hsm[];
@@ -160,7 +164,7 @@ __global__ void __launch_bounds__(288, 1) k_hess_tma(const T* __restrict__ A, in
   T* ring = reinterpret_cast<T*>(hsm);
   uint64_t* full = reinterpret_cast<uint64_t*>(hsm + align_up_dev(STAGES * stage_elems * sizeof(T), 128));
   uint64_t* empty = full + STAGES;
-  double* red = reinterpret_cast<double*>(empty + STAGES);  // [2][NW][R]
+  double* red = reinterpret_cast<double*>(empty + STAGES);  // [NX][2][NW][R], then ybuf [NX][2][R]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t row_begin = n * blockIdx.x / gridDim.x, row_end = n * (blockIdx.x + 1) / gridDim.x;
   const int64_t ntiles = (row_end - row_begin + R - 1) / R;
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(288, 1) k_hess_tma(const T* __restrict__ A, in
     return;
   }
   const int64_t nchunks = d / V;
-  double xv[NCH][V], acc[NCH][V];
+  double xv[NX][NCH][V], acc[NX][NCH][V];
   bool act[NCH];
 #pragma unroll
   for (int ch = 0; ch < NCH; ++ch) {
@@ -203,8 +207,12 @@ __global__ void __launch_bounds__(288, 1) k_hess_tma(const T* __restrict__ A, in
     act[ch] = c < nchunks;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      xv[ch][v] = act[ch] ? x[c * V + v] : 0.0;
-      acc[ch][v] = 0.0;
+#pragma unroll
+      for (int q = 0; q < NX; ++q) {
+        const double* xq = q == 0 ? x0 : x1;
+        xv[q][ch][v] = act[ch] ? xq[c * V + v] : 0.0;
+        acc[q][ch][v] = 0.0;
+      }
     }
   }
   int buf = 0;
@@ -222,15 +230,15 @@ __global__ void __launch_bounds__(288, 1) k_hess_tma(const T* __restrict__ A, in
         const int64_t c = (int64_t)ch * (NW * 32) + tid;
         if (r < rows && act[ch]) {
           if constexpr (sizeof(T) == 8) {
-            const double2 q = *reinterpret_cast<const double2*>(src + r * d + c * V);
-            a[r][ch][0] = q.x;
-            a[r][ch][1] = q.y;
+            const double2 qv = *reinterpret_cast<const double2*>(src + r * d + c * V);
+            a[r][ch][0] = qv.x;
+            a[r][ch][1] = qv.y;
           } else {
-            const float4 q = *reinterpret_cast<const float4*>(src + r * d + c * V);
-            a[r][ch][0] = q.x;
-            a[r][ch][1] = q.y;
-            a[r][ch][2] = q.z;
-            a[r][ch][3] = q.w;
+            const float4 qv = *reinterpret_cast<const float4*>(src + r * d + c * V);
+            a[r][ch][0] = qv.x;
+            a[r][ch][1] = qv.y;
+            a[r][ch][2] = qv.z;
+            a[r][ch][3] = qv.w;
           }
         } else {
 #pragma unroll
@@ -239,88 +247,97 @@ __global__ void __launch_bounds__(288, 1) k_hess_tma(const T* __restrict__ A, in
       }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // stage consumed by this warp
-    double dot[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if constexpr (sizeof(T) == 8) {
-        double sacc = 0.0;
+    for (int q = 0; q < NX; ++q) {
+      double dot[R];
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
+      for (int r = 0; r < R; ++r) {
+        if constexpr (sizeof(T) == 8) {
+          double sacc = 0.0;
 #pragma unroll
-          for (int v = 0; v < V; ++v) sacc = fma((double)a[r][ch][v], xv[ch][v], sacc);
-        dot[r] = sacc;
-      } else {
-        // fp32 data: short per-thread partial in fp32, reduced in fp64
-        float sacc = 0.0f;
+          for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
+            for (int v = 0; v < V; ++v) sacc = fma((double)a[r][ch][v], xv[q][ch][v], sacc);
+          dot[r] = sacc;
+        } else {
+          // fp32 data: short per-thread partial in fp32, reduced in fp64
+          float sacc = 0.0f;
 #pragma unroll
-          for (int v = 0; v < V; ++v) sacc = fmaf((float)a[r][ch][v], (float)xv[ch][v], sacc);
-        dot[r] = (double)sacc;
+          for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int v = 0; v < V; ++v) sacc = fmaf((float)a[r][ch][v], (float)xv[q][ch][v], sacc);
+          dot[r] = (double)sacc;
+        }
       }
-    }
-    {
       const double tot = warp_multi_sum<R>(dot);
-      if ((lane & (32 / R - 1)) == 0) red[(buf * NW + warp) * R + warp_multi_row<R>(lane)] = tot;
+      if ((lane & (32 / R - 1)) == 0) red[((q * 2 + buf) * NW + warp) * R + warp_multi_row<R>(lane)] = tot;
     }
     named_bar_sync(1, NW * 32);
-    double* ybuf = red + 2 * NW * R;  // [2][R]
-    if (tid < R) {
+    double* ybuf = red + NX * 2 * NW * R;  // [NX][2][R]
+    if (tid < NX * R) {
+      const int q = tid / R, r = tid - q * R;
       double y = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) y += red[(buf * NW + w) * R + tid];
-      ybuf[buf * R + tid] = y;
+      for (int w = 0; w < NW; ++w) y += red[((q * 2 + buf) * NW + w) * R + r];
+      ybuf[(q * 2 + buf) * R + r] = y;
     }
     named_bar_sync(1, NW * 32);
-    if constexpr (sizeof(T) == 8) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double y = ybuf[buf * R + r];
+    for (int q = 0; q < NX; ++q) {
+      if constexpr (sizeof(T) == 8) {
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
+        for (int r = 0; r < R; ++r) {
+          const double y = ybuf[(q * 2 + buf) * R + r];
 #pragma unroll
-          for (int v = 0; v < V; ++v) acc[ch][v] = fma(y, (double)a[r][ch][v], acc[ch][v]);
-      }
-    } else {
-      // the R-row rank update in fp32, folded into the fp64 accumulator once per stage
-      float st[NCH][V];
+          for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
-      for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-        for (int v = 0; v < V; ++v) st[ch][v] = 0.0f;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const float y = (float)ybuf[buf * R + r];
+            for (int v = 0; v < V; ++v) acc[q][ch][v] = fma(y, (double)a[r][ch][v], acc[q][ch][v]);
+        }
+      } else {
+        // the R-row rank update in fp32, folded into the fp64 accumulator once per stage
+        float stv[NCH][V];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
-          for (int v = 0; v < V; ++v) st[ch][v] = fmaf(y, (float)a[r][ch][v], st[ch][v]);
+          for (int v = 0; v < V; ++v) stv[ch][v] = 0.0f;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float y = (float)ybuf[(q * 2 + buf) * R + r];
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int v = 0; v < V; ++v) stv[ch][v] = fmaf(y, (float)a[r][ch][v], stv[ch][v]);
+        }
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[q][ch][v] += (double)stv[ch][v];
       }
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-        for (int v = 0; v < V; ++v) acc[ch][v] += (double)st[ch][v];
     }
     buf ^= 1;
   }
-  double* out = part + (int64_t)blockIdx.x * d;
 #pragma unroll
-  for (int ch = 0; ch < NCH; ++ch) {
-    if (!act[ch]) continue;
-    const int64_t c = (int64_t)ch * (NW * 32) + tid;
+  for (int q = 0; q < NX; ++q) {
+    double* out = (q == 0 ? part0 : part1) + (int64_t)blockIdx.x * d;
 #pragma unroll
-    for (int v = 0; v < V; ++v) out[c * V + v] = acc[ch][v];
+    for (int ch = 0; ch < NCH; ++ch) {
+      if (!act[ch]) continue;
+      const int64_t c = (int64_t)ch * (NW * 32) + tid;
+#pragma unroll
+      for (int v = 0; v < V; ++v) out[c * V + v] = acc[q][ch][v];
+    }
   }
 }
 
-template <typename T, int NCH, int R, int STAGES>
+template <typename T, int NCH, int R, int STAGES, int NX = 1>
 static int launch_tma(adask_ctx* ctx, const T* A, int64_t n, int64_t d, int64_t lda, const double* x,
-                      double* part, int grid, cudaStream_t st) {
+                      double* part, int grid, cudaStream_t st, const double* x1 = nullptr,
+                      double* part1 = nullptr) {
   const size_t ring = align_up((size_t)STAGES * R * d * sizeof(T), 128);
-  const size_t smem = ring + 2 * STAGES * sizeof(uint64_t) + (2 * 8 * R + 2 * R) * sizeof(double);
-  auto kern = k_hess_tma<T, NCH, R, STAGES>;
+  const size_t smem = ring + 2 * STAGES * sizeof(uint64_t) + NX * (2 * 8 * R + 2 * R) * sizeof(double);
+  auto kern = k_hess_tma<T, NCH, R, STAGES, NX>;
   ADASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, 288, smem, st>>>(A, n, d, lda, x, part);
+  kern<<<grid, 288, smem, st>>>(A, n, d, lda, x, x1, part, part1);
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;
 }
@@ -330,7 +347,7 @@ static int launch_tma(adask_ctx* ctx, const T* A, int64_t n, int64_t d, int64_t 
 template <typename T>
 static int hess_partial_tma(adask_ctx* ctx, const T* A, int64_t n, int64_t d, int64_t lda,
                             const double* x, double** part_out, int* nparts_out, cudaStream_t st,
-                            bool* used) {
+                            bool* used, const double* x1 = nullptr, double** part1_out = nullptr) {
   constexpr int V = 16 / sizeof(T);
   *used = false;
   if ((uintptr_t)A % 16 || (d % V) || (lda * (int64_t)sizeof(T)) % 16) return ADASK_OK;
@@ -338,14 +355,29 @@ static int hess_partial_tma(adask_ctx* ctx, const T* A, int64_t n, int64_t d, in
   int nch = (int)cdiv(nchunks, 256);
   if (nch > 8) return ADASK_OK;
   nch = nch <= 1 ? 1 : nch <= 2 ? 2 : nch <= 4 ? 4 : 8;
+  const bool pair = x1 != nullptr;
+  if (pair && nch > 4) return ADASK_OK;  // register budget of the two-column tile
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, cdiv(n, 16)));
   void* wsp = nullptr;
-  ADASK_TRY(ctx->ws[WS_HESS].get((size_t)grid * d * sizeof(double), st, &wsp));
+  ADASK_TRY(ctx->ws[WS_HESS].get((size_t)(pair ? 2 : 1) * grid * d * sizeof(double), st, &wsp));
   double* part = (double*)wsp;
+  double* part1 = pair ? part + (size_t)grid * d : nullptr;
   *part_out = part;
+  if (pair) *part1_out = part1;
   *nparts_out = grid;
   *used = true;
   const int64_t row_bytes = d * (int64_t)sizeof(T);
+  if (pair) {
+    switch (nch) {
+      case 1:
+        if (row_bytes <= 2048) return launch_tma<T, 1, 16, 6, 2>(ctx, A, n, d, lda, x, part, grid, st, x1, part1);
+        return launch_tma<T, 1, 8, 6, 2>(ctx, A, n, d, lda, x, part, grid, st, x1, part1);
+      case 2:
+        return launch_tma<T, 2, 4, 6, 2>(ctx, A, n, d, lda, x, part, grid, st, x1, part1);
+      default:
+        return launch_tma<T, 4, 2, 6, 2>(ctx, A, n, d, lda, x, part, grid, st, x1, part1);
+    }
+  }
   switch (nch) {
     case 1:
       if (row_bytes <= 2048) return launch_tma<T, 1, 16, 6>(ctx, A, n, d, lda, x, part, grid, st);
@@ -557,6 +589,31 @@ int hess_mult_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t 
                                                          out + j * ldo, partial ? 0 : 1);
     ADASK_LAUNCHED(ctx);
   }
+  return ADASK_OK;
+}
+
+// H [x0, x1] in one pass over A (c = 1 problems): out0 = H x0 (- B0), out1 =
+// H x1 (- B1); each column bitwise equal to hess_mult_impl's.  *fused = 0 when
+// the shape is not eligible (the caller then makes two single-column calls).
+int hess_mult_pair_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                        const double* x0, const double* B0, double* out0, const double* x1, const double* B1,
+                        double* out1, double nu2, const double* lam, cudaStream_t st, int* fused) {
+  *fused = 0;
+  if (n <= 0 || getenv("ADASK_NO_TMA") || getenv("ADASK_NO_PAIR")) return ADASK_OK;
+  ProfScope prof(ctx, PK_HESS, st, (double)n * d * (dtype == ADASK_F64 ? 8 : 4), 8.0 * (double)n * d);
+  double *part0 = nullptr, *part1 = nullptr;
+  int nparts = 0;
+  bool used = false;
+  if (dtype == ADASK_F64)
+    ADASK_TRY(hess_partial_tma<double>(ctx, (const double*)A, n, d, lda, x0, &part0, &nparts, st, &used, x1, &part1));
+  else
+    ADASK_TRY(hess_partial_tma<float>(ctx, (const float*)A, n, d, lda, x0, &part0, &nparts, st, &used, x1, &part1));
+  if (!used) return ADASK_OK;
+  k_hess_finish<<<(unsigned)cdiv(d, 32), 1024, 0, st>>>(part0, nparts, d, x0, nu2, lam, B0, out0, 1);
+  ADASK_LAUNCHED(ctx);
+  k_hess_finish<<<(unsigned)cdiv(d, 32), 1024, 0, st>>>(part1, nparts, d, x1, nu2, lam, B1, out1, 1);
+  ADASK_LAUNCHED(ctx);
+  *fused = 1;
   return ADASK_OK;
 }
 

@@ -9,4 +9,8 @@ int hess_mult_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t 
 int vec_hess_finish_impl(adask_ctx* ctx, const double* part, int64_t d, int64_t c, int64_t ld,
                          const double* X, double nu2, const double* lam, const double* B,
                          double* out, cudaStream_t st);
+// H [x0, x1] with one pass over A (see hessmult.cu); *fused = 0 if not eligible.
+int hess_mult_pair_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                        const double* x0, const double* B0, double* out0, const double* x1, const double* B1,
+                        double* out1, double nu2, const double* lam, cudaStream_t st, int* fused);
 }  // namespace adask

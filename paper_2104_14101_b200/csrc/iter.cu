@@ -188,6 +188,84 @@ static int check_problem(const adask_problem* pb) {
   return ADASK_OK;
 }
 
+__global__ void k_negate_copy(const double* __restrict__ a, double* __restrict__ out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = -a[i];
+}
+
+// PCG proposal that also leaves H x - B (x = the current iterate) in hx_mb when
+// the pass over A can serve both columns (*hx_ok = 1): a rejected proposal's
+// restart then needs no second pass (pcg_restart_impl with hx_mb).  Every
+// value is bitwise the one adask_pcg_propose / adask_pcg_restart compute.
+int pcg_propose_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P, const double* x,
+                     const double* r, const double* p, const double* dt_col, double* Hp, double* x_new,
+                     double* r_new, double* rt_new, double* dt_new, double* delta_tilde_host, double* hx_mb,
+                     int* hx_ok, cudaStream_t st) {
+  ADASK_TRY(check_problem(pb));
+  const int64_t d = pb->d, c = pb->c;
+  *hx_ok = 0;
+  if (hx_mb && !pb->allreduce && c == 1)
+    ADASK_TRY(hess_mult_pair_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, nullptr, Hp, x, pb->B, hx_mb,
+                                  pb->nu2, pb->lam, st, hx_ok));
+  if (!*hx_ok) ADASK_TRY(problem_hess(ctx, pb, p, nullptr, Hp, st));
+  IterScalars* sc = nullptr;
+  ADASK_TRY(get_scalars(ctx, &sc, st));
+  k_pcg_step<<<1, kVecThreads, 0, st>>>(d, c, x, r, p, Hp, dt_col, x_new, r_new, sc);
+  ADASK_LAUNCHED(ctx);
+  ADASK_TRY(precond_apply_impl(ctx, P, r_new, c, d, rt_new, d, st));
+  k_pcg_scalars<<<1, kVecThreads, 0, st>>>(d, c, r_new, rt_new, dt_new, sc);
+  ADASK_LAUNCHED(ctx);
+  int flags = 0;
+  ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
+  if (flags & FLAG_BREAKDOWN) return fail(ADASK_E_BREAKDOWN, "direction with nonpositive curvature");
+  if (flags & FLAG_NEGATIVE) return fail(ADASK_E_NEGATIVE, "r.T H_S^-1 r went negative beyond roundoff");
+  return ADASK_OK;
+}
+
+// PCG restart; hx_mb = H x - B from the proposal's fused pass, or null.
+int pcg_restart_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P, const double* x,
+                     double* r, double* rt, double* p, double* dt_col, double* delta_tilde_host,
+                     const double* hx_mb, cudaStream_t st) {
+  ADASK_TRY(check_problem(pb));
+  const int64_t d = pb->d, c = pb->c;
+  if (hx_mb) {
+    k_negate_copy<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(hx_mb, r, d * c);
+    ADASK_LAUNCHED(ctx);
+  } else {
+    // r = B - H x   (computed as -(H x - B), exact)
+    ADASK_TRY(problem_hess(ctx, pb, x, pb->B, r, st));
+    k_negate<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(r, d * c);
+    ADASK_LAUNCHED(ctx);
+  }
+  ADASK_TRY(precond_apply_impl(ctx, P, r, c, d, rt, d, st));
+  IterScalars* sc = nullptr;
+  ADASK_TRY(get_scalars(ctx, &sc, st));
+  k_pcg_restart_tail<<<1, kVecThreads, 0, st>>>(d, c, rt, r, p, dt_col, sc);
+  ADASK_LAUNCHED(ctx);
+  int flags = 0;
+  ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
+  if (flags & FLAG_NEGATIVE) return fail(ADASK_E_NEGATIVE, "r.T H_S^-1 r went negative beyond roundoff");
+  return ADASK_OK;
+}
+
+// IHS restart; have_g: g already holds grad f(x) = H x - B (computed by the
+// proposal that produced x, or by the previous restart at the same x -- the
+// same kernel on the same x, so the same bits the reference's recomputation
+// would give), and the pass over A is skipped.
+int ihs_restart_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precond* P, const double* x, double* g,
+                     double* v, double* delta_tilde_host, bool have_g, cudaStream_t st) {
+  ADASK_TRY(check_problem(pb));
+  const int64_t d = pb->d, c = pb->c;
+  if (!have_g) ADASK_TRY(problem_hess(ctx, pb, x, pb->B, g, st));
+  ADASK_TRY(precond_apply_impl(ctx, P, g, c, d, v, d, st));
+  IterScalars* sc = nullptr;
+  ADASK_TRY(get_scalars(ctx, &sc, st));
+  k_half_dot<<<1, kVecThreads, 0, st>>>(d, c, d, g, v, sc);
+  ADASK_LAUNCHED(ctx);
+  int flags = 0;
+  return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
+}
+
 }  // namespace adask
 
 using namespace adask;
