@@ -86,6 +86,12 @@ int chol_factor_inverse(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t k
     ADASK_TRY(chol64::launch(ctx, dtype, M, k, kp, L, Li, LiT, info, tlog, st, &grid));
   else
     ADASK_TRY(chol32::launch(ctx, dtype, M, k, kp, L, Li, LiT, info, tlog, st, &grid));
+  if (ctx->defer_spd && !trace) {
+    // the driver reads pinned_flags[1] after its next synchronization
+    ADASK_CUDA(cudaMemcpyAsync(ctx->pinned_flags + 1, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (info_host) *info_host = 0;
+    return ADASK_OK;
+  }
   ADASK_CUDA(cudaMemcpyAsync(ctx->pinned_flags, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   ADASK_CUDA(cudaStreamSynchronize(st));
   if (trace) {

@@ -126,6 +126,9 @@ struct adask_ctx {
   std::vector<adask_prof_rec> prof_recs[adask::PK_COUNT];
   std::vector<cudaEvent_t> event_pool;
   void* blas = nullptr;  // cublasHandle_t, created on first Gram (gram.cu)
+  // native driver: the Cholesky's pivot check is read at the driver's next
+  // stream synchronization instead of a sync of its own (pinned_flags[1])
+  bool defer_spd = false;
 };
 
 namespace adask {

@@ -295,6 +295,25 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
     return ADASK_OK;
   };
 
+  // Cholesky pivot checks are read after each restart's synchronization (the
+  // reference raises NotPositiveDefinite from build; reported here before any
+  // error the restart itself may raise from the unusable factor)
+  struct DeferGuard {
+    adask_ctx* c;
+    bool old;
+    ~DeferGuard() { c->defer_spd = old; }
+  } dguard{ctx, ctx->defer_spd};
+  ctx->defer_spd = getenv("ADASK_NO_DEFER_SPD") == nullptr;
+  ctx->pinned_flags[1] = 0;
+  auto spd_check = [&]() -> int {
+    const int h = ctx->pinned_flags[1];
+    if (h != 0) {
+      ctx->pinned_flags[1] = 0;
+      return fail(ADASK_E_NOT_SPD, "Matrix is not positive definite (leading minor %d)", h);
+    }
+    return ADASK_OK;
+  };
+
   // sketch + build
   // SA buffers: two grow-only context workspaces (the live preconditioner
   // references the current one; the next sketch goes to the other), so
@@ -344,7 +363,11 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
     if (polyak) ADASK_CUDA(cudaMemcpyAsync(xp, x, cd * sizeof(double), cudaMemcpyDeviceToDevice, st));
     return ADASK_OK;
   };
-  ADASK_TRY(restart());
+  {
+    const int rs = restart();
+    ADASK_TRY(spd_check());
+    ADASK_TRY(rs);
+  }
   const double dt_first = delta;
   double dt_I = delta;
   int64_t t = 0, I = 0;
@@ -382,7 +405,11 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
       sa_slot = nslot;
       ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
                                     (void*)st));
-      ADASK_TRY(restart());
+      {
+        const int rs = restart();
+        ADASK_TRY(spd_check());
+        ADASK_TRY(rs);
+      }
       dt_I = delta;
       I = t;
       ADASK_TRY(record(t, m, K, dt_I, x, ADASK_EV_RESKETCH));

@@ -249,3 +249,21 @@ def test_incremental_tf32_gaussian_converges():
     assert tr.records[-1].delta_exact <= 1e-6 * d0
     ms = [m for _, m in tr.schedule()]
     assert ms == sorted(ms) and all(b == 2 * a for a, b in zip([8] + ms[:-1], ms))
+
+
+@pytest.mark.parametrize("method", ["pcg", "ihs"])
+def test_native_driver_reports_not_positive_definite(method):
+    """The native driver reads the Cholesky pivot check after the restart's
+    synchronization (no sync of its own); a non-finite sketch still raises
+    NotPositiveDefinite, as the reference's build does (preconditioner.py:60-74)."""
+    import paper_2104_14101_b200 as ak
+    from paper_2104_14101_b200.errors import NotPositiveDefinite
+
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((2048, 40))
+    A[77, 3] = np.nan
+    b = rng.standard_normal(40)
+    p = ak.RegularizedProblem(A, b, 1e-1, None, validate=False)
+    cfg = ak.AdaptiveConfig.for_method(method, 0.125, 8, 4, "sjlt", 1)
+    with pytest.raises(NotPositiveDefinite):
+        ak.adaptive_run(p, np.zeros(40), cfg, method=method, native=True)

@@ -47,18 +47,18 @@ if os.environ.get("TIME", "1") == "1":
     A = torch.randn(n, d, dtype=torch.float64, device="cuda")
     for m in (32, 256, 1024, 4096):
         for pipe in (False, True, 2):
-            os.environ["ADASK_FWHT_IP"] = "0" if pipe == 2 else "1"
+            os.environ["ADASK_FWHT_LDG"] = "0" if pipe == 2 else "1"
             ms = t(lambda: run(A, m, 7, pipe))
-            print(f"srht{(' ip' if pipe is True else ' scratch') if pipe else ' tile'} n={n} d={d} m={m}: {ms*1e3:.1f} us  "
+            print(f"srht{(" ldg" if pipe is True else " tma") if pipe else ' tile'} n={n} d={d} m={m}: {ms*1e3:.1f} us  "
                   f"{(n+m)*d*8/ms/1e6:.0f} GB/s", flush=True)
     del A
     n, d = 1 << 21, 1024
     A = torch.randn(n, d, dtype=torch.float32, device="cuda")
     for m in (64, 1024, 4096, 32768):
         for pipe in (False, True, 2):
-            os.environ["ADASK_FWHT_IP"] = "0" if pipe == 2 else "1"
+            os.environ["ADASK_FWHT_LDG"] = "0" if pipe == 2 else "1"
             ms = t(lambda: run(A, m, 7, pipe), 3)
-            print(f"srht{(' ip' if pipe is True else ' scratch') if pipe else ' tile'} fp32 n={n} d={d} m={m}: {ms*1e3:.1f} us  "
+            print(f"srht{(" ldg" if pipe is True else " tma") if pipe else ' tile'} fp32 n={n} d={d} m={m}: {ms*1e3:.1f} us  "
                   f"{(n+m)*d*4/ms/1e6:.0f} GB/s", flush=True)
 
 if os.environ.get("B1SWEEP", "0") == "1":
