@@ -313,8 +313,7 @@ def run_ours(args) -> None:
         solve()
     _log("timed solves")
     ctx = dv.ctx()
-    ctx.prof_reset()
-    ctx.prof_enable(True)
+    ctx.prof_enable(False)
     launches0 = ctx.launches()
     torch.cuda.synchronize()
     if dist:
@@ -336,8 +335,22 @@ def run_ours(args) -> None:
     if dist:
         dist.barrier()
     launches = ctx.launches() - launches0
+    # per-unit kernel times (roofline, `units`): a second pass of the same K
+    # steps with a CUDA event pair around every unit on the launching stream
+    # (the events cost ~5% of a config-1 step, so `value` is taken without them)
+    _log("profiled pass (per-unit CUDA events)")
+    ctx.prof_reset()
+    ctx.prof_enable(True)
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for k in range(args.steps):
+        solve()
+    p1.record()
+    torch.cuda.synchronize()
     ctx.prof_enable(False)
     prof = ctx.prof_query()
+    prof_ms_per_step = p0.elapsed_time(p1) / args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     if dist:
         t = torch.tensor([ms], device=dev)
@@ -443,6 +456,9 @@ def run_ours(args) -> None:
             "solves_per_s_total": (ws if cfg.index < 2 else 1) * 1e3 / ms,
             "sketch_gbs": sketch_gbs,
             "units": units,
+            "units_pass": {"ms_per_step": prof_ms_per_step,
+                           "note": "units and roofline from a second pass of the same steps with per-unit CUDA "
+                                   "events on the launching stream; value/ms_per_step from the pass without them"},
             "roofline": {"bound": bound, "unit_name": dom, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,
                          "per_launch_ms": per_launch_ms, "alg_work_per_launch": work_per,

@@ -386,6 +386,21 @@ int64_t adask_ctx_launches(const adask_ctx* ctx) { return ctx ? ctx->launches : 
 extern "C" int adask_prof_enable(adask_ctx* ctx, int on) {
   if (!ctx) return fail(ADASK_E_ARG, "null context");
   ctx->prof = on ? 1 : 0;
+  if (on) {
+    // create the timing events up front: a cudaEventCreate inside a timed
+    // region costs microseconds of host time per unit
+    cudaSetDevice(ctx->device);
+    size_t live = 0;
+    for (auto& v : ctx->prof_recs) live += 2 * v.size();
+    while (ctx->event_pool.size() + live < 8192) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        cudaGetLastError();
+        break;
+      }
+      ctx->event_pool.push_back(e);
+    }
+  }
   return ADASK_OK;
 }
 
