@@ -492,11 +492,12 @@ inline int launch(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, voi
   CholArgs a{M, L, Li, LiT, (int)kp, nblk, (int)k, info, tlog, getenv("ADASK_CHOL_SLOWDIAG") ? 1 : 0};
   const int smem = 3 * NB * NBP * (int)sizeof(double);
   void* fn = dtype == ADASK_F64 ? (void*)k_chol_coop<double> : (void*)k_chol_coop<float>;
-  ADASK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  int per_sm = 0;
-  ADASK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCholThreads, smem));
-  int nsm = kNumSMs;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+  ADASK_TRY(ensure_smem_attr(fn, smem));
+  static int per_sm_cache[2] = {-1, -1}, nsm_cache = -1;  // per dtype; one device type per process
+  int& per_sm = per_sm_cache[dtype == ADASK_F64 ? 0 : 1];
+  if (per_sm < 0) ADASK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCholThreads, smem));
+  if (nsm_cache < 0) cudaDeviceGetAttribute(&nsm_cache, cudaDevAttrMultiProcessorCount, ctx->device);
+  int nsm = nsm_cache;
   if (per_sm < 1) return fail(ADASK_E_CUDA, "chol: kernel cannot be resident");
   int grid = nsm;  // one CTA per SM
   const int maxwork = nblk * (nblk + 1) / 2;

@@ -132,6 +132,10 @@ struct adask_ctx {
 };
 
 namespace adask {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the driver call costs microseconds of host time, and on the per-iteration
+// path the GPU idles while the host issues the next kernel.
+int ensure_smem_attr(const void* fn, int bytes);
 // RAII timing scope for one unit; no-op unless profiling is enabled.
 struct ProfScope {
   adask_ctx* ctx;

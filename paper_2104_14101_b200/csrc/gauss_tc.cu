@@ -369,7 +369,7 @@ int launch_tc(adask_ctx* ctx, const CUtensorMap& map, int64_t n_local, int64_t d
   using C = TcCfg<NH>;
   static bool attr = false;
   if (!attr) {
-    ADASK_CUDA(cudaFuncSetAttribute(k_gauss_tc<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    ADASK_TRY(ensure_smem_attr((const void*)k_gauss_tc<NH>, C::SMEM));
     attr = true;
   }
   const float scale = (float)(1.0 / sqrt((double)m_total));

@@ -336,7 +336,7 @@ static int launch_tma(adask_ctx* ctx, const T* A, int64_t n, int64_t d, int64_t 
   const size_t ring = align_up((size_t)STAGES * R * d * sizeof(T), 128);
   const size_t smem = ring + 2 * STAGES * sizeof(uint64_t) + NX * (2 * 8 * R + 2 * R) * sizeof(double);
   auto kern = k_hess_tma<T, NCH, R, STAGES, NX>;
-  ADASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ADASK_TRY(ensure_smem_attr((const void*)kern, (int)smem));
   kern<<<grid, 288, smem, st>>>(A, n, d, lda, x, x1, part, part1);
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;

@@ -1,3 +1,5 @@
+#include <map>
+#include <mutex>
 // Host side of libadask: error state, device context, and the numpy-exact
 // seeding / PCG64 / bounded-integer / choice bookkeeping that decides which
 // rows a sketch touches.  None of this is floating-point compute: it is the
@@ -382,6 +384,22 @@ int adask_ctx_destroy(adask_ctx* ctx) {
 int64_t adask_ctx_launches(const adask_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 }  // extern "C"
+
+namespace adask {
+int ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{fn, dev}];
+  if (have >= bytes) return ADASK_OK;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return fail(ADASK_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  have = bytes;
+  return ADASK_OK;
+}
+}  // namespace adask
 
 extern "C" int adask_prof_enable(adask_ctx* ctx, int on) {
   if (!ctx) return fail(ADASK_E_ARG, "null context");

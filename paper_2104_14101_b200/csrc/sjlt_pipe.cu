@@ -218,10 +218,10 @@ int sjlt_accumulate_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t d, in
   const size_t smem = (size_t)a.stages * a.stage_bytes + (size_t)a.stages * (16 + 4) + 64;
   const int grid = (int)std::min<int64_t>(m * a.npanels, kNumSMs);
   if (dtype == ADASK_F64) {
-    ADASK_CUDA(cudaFuncSetAttribute(k_sjlt_pipe<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ADASK_TRY(ensure_smem_attr((const void*)k_sjlt_pipe<double>, (int)smem));
     k_sjlt_pipe<double><<<grid, kThreads, smem, st>>>(a);
   } else {
-    ADASK_CUDA(cudaFuncSetAttribute(k_sjlt_pipe<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ADASK_TRY(ensure_smem_attr((const void*)k_sjlt_pipe<float>, (int)smem));
     k_sjlt_pipe<float><<<grid, kThreads, smem, st>>>(a);
   }
   ADASK_LAUNCHED(ctx);

@@ -261,7 +261,7 @@ static int launch_fw(adask_ctx* ctx, const FwhtArgs& a, int64_t nblk, cudaStream
   constexpr int B = 1 << LOG;
   size_t smem = fw_tile_bytes<T, LOG>() + sizeof(int) * (size_t)B;
   auto kern = k_fwht_tile<T, LOG, MODE>;
-  if (smem > 48 * 1024) ADASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) ADASK_TRY(ensure_smem_attr((const void*)kern, (int)smem));
   dim3 grid((unsigned)cdiv(a.d, C), (unsigned)nblk);
   kern<<<grid, 256, smem, st>>>(a);
   ADASK_LAUNCHED(ctx);

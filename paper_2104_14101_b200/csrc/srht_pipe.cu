@@ -513,7 +513,7 @@ int launch_pipe(adask_ctx* ctx, int dtype, const void* src, int64_t rows, int64_
   a.npanels = cdiv(a.d, S::W);
   a.n_items = cdiv(tile_rows, S::BT) * a.npanels;
   auto kern = k_fwht_pipe<T, LOG, LOGT, SEGB, MODE>;
-  ADASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+  ADASK_TRY(ensure_smem_attr((const void*)kern, (int)S::SMEM));
   const int grid = (int)std::min<int64_t>(a.n_items, kNumSMs);
   kern<<<grid, kThreads, S::SMEM, st>>>(map, a);
   ADASK_LAUNCHED(ctx);
