@@ -431,6 +431,46 @@ __global__ void __launch_bounds__(1024) k_hess_finish(const double* __restrict__
   }
 }
 
+// Both columns of a pair pass in one launch (blockIdx.y = column).
+__global__ void __launch_bounds__(1024) k_hess_finish_pair(const double* __restrict__ part0,
+                                                           const double* __restrict__ part1, int nparts, int64_t d,
+                                                           const double* __restrict__ x0,
+                                                           const double* __restrict__ x1, double nu2,
+                                                           const double* __restrict__ lam,
+                                                           const double* __restrict__ B0,
+                                                           const double* __restrict__ B1, double* __restrict__ out0,
+                                                           double* __restrict__ out1) {
+  const bool q = blockIdx.y != 0;
+  const double* part = q ? part1 : part0;
+  const double* x = q ? x1 : x0;
+  const double* B = q ? B1 : B0;
+  double* out = q ? out1 : out0;
+  __shared__ double sh[32][33];
+  const int cx = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + cx;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (j < d) {
+    int b = g;
+    for (; b + 96 < nparts; b += 128) {
+      s0 += part[(int64_t)b * d + j];
+      s1 += part[(int64_t)(b + 32) * d + j];
+      s2 += part[(int64_t)(b + 64) * d + j];
+      s3 += part[(int64_t)(b + 96) * d + j];
+    }
+    for (; b < nparts; b += 32) s0 += part[(int64_t)b * d + j];
+  }
+  sh[g][cx] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (g == 0 && j < d) {
+    double t = sh[0][cx];
+#pragma unroll
+    for (int r = 1; r < 32; ++r) t += sh[r][cx];
+    t += nu2 * (lam[j] * x[j]);
+    if (B) t -= B[j];
+    out[j] = t;
+  }
+}
+
 // Two-pass path for rows too wide for the fused register tile:
 // y = A x (warp per row), then column-parallel A^T y partials.
 template <typename T>
@@ -611,9 +651,8 @@ int hess_mult_pair_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int
   else
     ADASK_TRY(hess_partial_tma<float>(ctx, (const float*)A, n, d, lda, x0, &part0, &nparts, st, &used, x1, &part1));
   if (!used) return ADASK_OK;
-  k_hess_finish<<<(unsigned)cdiv(d, 32), 1024, 0, st>>>(part0, nparts, d, x0, nu2, lam, B0, out0, 1);
-  ADASK_LAUNCHED(ctx);
-  k_hess_finish<<<(unsigned)cdiv(d, 32), 1024, 0, st>>>(part1, nparts, d, x1, nu2, lam, B1, out1, 1);
+  k_hess_finish_pair<<<dim3((unsigned)cdiv(d, 32), 2), 1024, 0, st>>>(part0, part1, nparts, d, x0, x1, nu2, lam,
+                                                                       B0, B1, out0, out1);
   ADASK_LAUNCHED(ctx);
   *fused = 1;
   return ADASK_OK;
