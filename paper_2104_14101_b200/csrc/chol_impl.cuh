@@ -48,6 +48,39 @@ __device__ __forceinline__ void tile_load(double (*s)[NBP], const T* base, int l
   }
 }
 
+// Split tile load: global -> registers (fetch, issued early) and registers ->
+// SMEM (put), so the next tile's loads overlap the current tile product.
+template <typename T>
+struct TileRegs {
+  using VT = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  static constexpr int V = 16 / sizeof(T);
+  static constexpr int PER = NB * NB / V / kCholThreads;
+  VT v[PER];
+};
+template <typename T>
+__device__ __forceinline__ void tile_fetch(TileRegs<T>& R, const T* base, int ld, int bi, int bj) {
+  using X = TileRegs<T>;
+  const T* p = base + (int64_t)bi * NB * ld + (int64_t)bj * NB;
+#pragma unroll
+  for (int q = 0; q < X::PER; ++q) {
+    const int idx = threadIdx.x + kCholThreads * q;
+    const int r = idx / (NB / X::V), c = (idx % (NB / X::V)) * X::V;
+    R.v[q] = *reinterpret_cast<const typename X::VT*>(p + (int64_t)r * ld + c);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void tile_put(double (*s)[NBP], const TileRegs<T>& R) {
+  using X = TileRegs<T>;
+#pragma unroll
+  for (int q = 0; q < X::PER; ++q) {
+    const int idx = threadIdx.x + kCholThreads * q;
+    const int r = idx / (NB / X::V), c = (idx % (NB / X::V)) * X::V;
+    const T* e = reinterpret_cast<const T*>(&R.v[q]);
+#pragma unroll
+    for (int u = 0; u < X::V; ++u) s[r][c + u] = (double)e[u];
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void tile_store(T* base, int ld, int bi, int bj, const double (*s)[NBP],
                                            bool transpose = false, int lower_only = 0) {
@@ -321,6 +354,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
   double(*sA)[NBP] = reinterpret_cast<double(*)[NBP]>(csm);
   double(*sB)[NBP] = reinterpret_cast<double(*)[NBP]>(csm + NB * NBP);
   double(*sC)[NBP] = reinterpret_cast<double(*)[NBP]>(csm + 2 * NB * NBP);
+  double(*sD)[NBP] = reinterpret_cast<double(*)[NBP]>(csm + 3 * NB * NBP);  // second buffers of the
+  double(*sE)[NBP] = reinterpret_cast<double(*)[NBP]>(csm + 4 * NB * NBP);  // pipelined inverse
   T* M = reinterpret_cast<T*>(a.M);
   T* L = reinterpret_cast<T*>(a.L);
   T* Li = reinterpret_cast<T*>(a.Li);
@@ -428,11 +463,24 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
       }
       const int i = b0 + s + tt / s, l = b0 + tt % s;
       acc_zero(acc);
-      for (int p = l; p < b0 + s; ++p) {
-        tile_load<T>(sA, L, ld, i, p);
-        tile_load<T>(sB, Li, ld, p, l);
-        __syncthreads();
-        tile_mma<false>(sA, sB, acc);
+      {
+        // double-buffered: the next (L, Li) tile pair is in flight during
+        // the current product; one barrier per product
+        TileRegs<T> ra, rb;
+        tile_fetch<T>(ra, L, ld, i, l);
+        tile_fetch<T>(rb, Li, ld, l, l);
+        int cur = 0;
+        for (int p = l; p < b0 + s; ++p) {
+          tile_put<T>(cur ? sD : sA, ra);
+          tile_put<T>(cur ? sE : sB, rb);
+          __syncthreads();
+          if (p + 1 < b0 + s) {
+            tile_fetch<T>(ra, L, ld, i, p + 1);
+            tile_fetch<T>(rb, Li, ld, p + 1, l);
+          }
+          tile_mma<false>(cur ? sD : sA, cur ? sE : sB, acc);
+          cur ^= 1;
+        }
         __syncthreads();
       }
       acc_to_tile(sC, acc, 1.0);
@@ -453,11 +501,22 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
       }
       const int i = b0 + s + tt / s, l = b0 + tt % s;
       acc_zero(acc);
-      for (int p = b0 + s; p <= i; ++p) {
-        tile_load<T>(sA, Li, ld, i, p);
-        tile_load<T>(sB, M, ld, p, l);
-        __syncthreads();
-        tile_mma<false>(sA, sB, acc);
+      {
+        TileRegs<T> ra, rb;
+        tile_fetch<T>(ra, Li, ld, i, b0 + s);
+        tile_fetch<T>(rb, M, ld, b0 + s, l);
+        int cur = 0;
+        for (int p = b0 + s; p <= i; ++p) {
+          tile_put<T>(cur ? sD : sA, ra);
+          tile_put<T>(cur ? sE : sB, rb);
+          __syncthreads();
+          if (p + 1 <= i) {
+            tile_fetch<T>(ra, Li, ld, i, p + 1);
+            tile_fetch<T>(rb, M, ld, p + 1, l);
+          }
+          tile_mma<false>(cur ? sD : sA, cur ? sE : sB, acc);
+          cur ^= 1;
+        }
         __syncthreads();
       }
       acc_to_tile(sC, acc, -1.0);
@@ -490,7 +549,7 @@ inline int launch(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, voi
                   int* info, unsigned long long* tlog, cudaStream_t st, int* grid_out) {
   const int nblk = (int)(kp / NB);
   CholArgs a{M, L, Li, LiT, (int)kp, nblk, (int)k, info, tlog, getenv("ADASK_CHOL_SLOWDIAG") ? 1 : 0};
-  const int smem = 3 * NB * NBP * (int)sizeof(double);
+  const int smem = 5 * NB * NBP * (int)sizeof(double);
   void* fn = dtype == ADASK_F64 ? (void*)k_chol_coop<double> : (void*)k_chol_coop<float>;
   ADASK_TRY(ensure_smem_attr(fn, smem));
   static int per_sm_cache[2] = {-1, -1}, nsm_cache = -1;  // per dtype; one device type per process
