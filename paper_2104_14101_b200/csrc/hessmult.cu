@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(1024) k_hess_finish_pair(const double* __restr
                                                            const double* __restrict__ lam,
                                                            const double* __restrict__ B0,
                                                            const double* __restrict__ B1, double* __restrict__ out0,
-                                                           double* __restrict__ out1) {
+                                                           double* __restrict__ out1, int epilogue) {
   const bool q = blockIdx.y != 0;
   const double* part = q ? part1 : part0;
   const double* x = q ? x1 : x0;
@@ -465,8 +465,10 @@ __global__ void __launch_bounds__(1024) k_hess_finish_pair(const double* __restr
     double t = sh[0][cx];
 #pragma unroll
     for (int r = 1; r < 32; ++r) t += sh[r][cx];
-    t += nu2 * (lam[j] * x[j]);
-    if (B) t -= B[j];
+    if (epilogue) {
+      t += nu2 * (lam[j] * x[j]);
+      if (B) t -= B[j];
+    }
     out[j] = t;
   }
 }
@@ -639,7 +641,7 @@ int hess_mult_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t 
 // the shape is not eligible (the caller then makes two single-column calls).
 int hess_mult_pair_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                         const double* x0, const double* B0, double* out0, const double* x1, const double* B1,
-                        double* out1, double nu2, const double* lam, cudaStream_t st, int* fused) {
+                        double* out1, double nu2, const double* lam, cudaStream_t st, int* fused, int partial) {
   *fused = 0;
   if (n <= 0 || getenv("ADASK_NO_TMA") || getenv("ADASK_NO_PAIR")) return ADASK_OK;
   ProfScope prof(ctx, PK_HESS, st, (double)n * d * (dtype == ADASK_F64 ? 8 : 4), 8.0 * (double)n * d);
@@ -652,7 +654,7 @@ int hess_mult_pair_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int
     ADASK_TRY(hess_partial_tma<float>(ctx, (const float*)A, n, d, lda, x0, &part0, &nparts, st, &used, x1, &part1));
   if (!used) return ADASK_OK;
   k_hess_finish_pair<<<dim3((unsigned)cdiv(d, 32), 2), 1024, 0, st>>>(part0, part1, nparts, d, x0, x1, nu2, lam,
-                                                                       B0, B1, out0, out1);
+                                                                       B0, B1, out0, out1, partial ? 0 : 1);
   ADASK_LAUNCHED(ctx);
   *fused = 1;
   return ADASK_OK;

@@ -204,9 +204,24 @@ int pcg_propose_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precon
   ADASK_TRY(check_problem(pb));
   const int64_t d = pb->d, c = pb->c;
   *hx_ok = 0;
-  if (hx_mb && !pb->allreduce && c == 1)
-    ADASK_TRY(hess_mult_pair_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, nullptr, Hp, x, pb->B, hx_mb,
-                                  pb->nu2, pb->lam, st, hx_ok));
+  if (hx_mb && c == 1) {
+    if (!pb->allreduce) {
+      ADASK_TRY(hess_mult_pair_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, nullptr, Hp, x, pb->B, hx_mb,
+                                    pb->nu2, pb->lam, st, hx_ok));
+    } else if (pb->n > 0) {
+      // row-sharded: the pair of partial A_g^T A_g [p, x], all-reduced, then
+      // the regularizer / B epilogues (problem_hess's sequence per column)
+      ADASK_TRY(hess_mult_pair_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, nullptr, Hp, x, nullptr, hx_mb,
+                                    pb->nu2, pb->lam, st, hx_ok, 1));
+      if (*hx_ok) {
+        if (pb->allreduce(Hp, d, ADASK_F64, pb->allreduce_user, (void*)st) != 0 ||
+            pb->allreduce(hx_mb, d, ADASK_F64, pb->allreduce_user, (void*)st) != 0)
+          return fail(ADASK_E_CUDA, "all-reduce of the partial A^T A [p, x] failed");
+        ADASK_TRY(vec_hess_finish_impl(ctx, Hp, d, 1, d, p, pb->nu2, pb->lam, nullptr, Hp, st));
+        ADASK_TRY(vec_hess_finish_impl(ctx, hx_mb, d, 1, d, x, pb->nu2, pb->lam, pb->B, hx_mb, st));
+      }
+    }
+  }
   if (!*hx_ok) ADASK_TRY(problem_hess(ctx, pb, p, nullptr, Hp, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));

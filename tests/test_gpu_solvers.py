@@ -114,6 +114,14 @@ def test_sharded_problem_allreduce_hook_world1():
         x1, tr1 = ak.adaptive_run(p, np.zeros(128), cfg)
         assert _events(tr) == _events(tr1)
         assert np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
+        # the native driver on the sharded problem: the all-reduce hook inside
+        # the two-column proposal pass (restart reuse) and the sketches
+        for method in ("pcg", "ihs"):
+            cfg_m = ak.AdaptiveConfig.for_method(method, 0.125, 8, 8, "sjlt", 1)
+            xn, trn = ak.adaptive_run(ps, np.zeros(128), cfg_m, method=method, native=True)
+            xr, trr = ak.adaptive_run(p, np.zeros(128), cfg_m, method=method)
+            assert _events(trn) == _events(trr)
+            assert np.linalg.norm(xn - xr) <= 1e-10 * np.linalg.norm(xr)
     finally:
         dist.destroy_process_group()
 
