@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const T* __restrict__ M, int6
                                                    int64_t cols, int64_t ld,
                                                    const double* __restrict__ x, double alpha,
                                                    double* __restrict__ out, int mode, int vec) {
+  pdl_wait();
   constexpr int CE = 16 / (int)sizeof(T);  // elements per 16-byte chunk
   constexpr int U = 8;
   const int lane = threadIdx.x & 31;
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(256) k_gemv_rows(const T* __restrict__ M, int6
 template <typename T>
 __global__ void k_gemv_cols(const T* __restrict__ M, int64_t rows, int64_t cols, int64_t ld,
                             const double* __restrict__ u, double* __restrict__ part) {
+  pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int nb = gridDim.y;
   const int64_t r0 = rows * blockIdx.y / nb, r1 = rows * (blockIdx.y + 1) / nb;
@@ -103,6 +105,7 @@ __global__ void k_gemv_cols(const T* __restrict__ M, int64_t rows, int64_t cols,
 __global__ void k_woodbury_finish(const double* __restrict__ part, int nb, int64_t d,
                                   const double* __restrict__ y, const double* __restrict__ lam,
                                   double nu2, double* __restrict__ out) {
+  pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d) return;
   double s = 0.0;
@@ -112,6 +115,7 @@ __global__ void k_woodbury_finish(const double* __restrict__ part, int nb, int64
 
 __global__ void k_div_vec(const double* __restrict__ z, const double* __restrict__ lam, int64_t d,
                           double* __restrict__ y) {
+  pdl_wait();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < d) y[j] = z[j] / lam[j];
 }
@@ -123,9 +127,11 @@ int gemv_rows(adask_ctx* ctx, int dtype, const void* M, int64_t rows, int64_t co
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
   const int vec = ((uintptr_t)M % 16 == 0) && ((size_t)ld * esz) % 16 == 0;
   if (dtype == ADASK_F64)
-    k_gemv_rows<double><<<blocks, 256, 0, st>>>((const double*)M, rows, cols, ld, x, alpha, out, mode, vec);
+    ADASK_CUDA(launch_pdl(k_gemv_rows<double>, dim3(blocks), dim3(256), 0, st, (const double*)M, rows, cols, ld, x,
+                          alpha, out, mode, vec));
   else
-    k_gemv_rows<float><<<blocks, 256, 0, st>>>((const float*)M, rows, cols, ld, x, alpha, out, mode, vec);
+    ADASK_CUDA(launch_pdl(k_gemv_rows<float>, dim3(blocks), dim3(256), 0, st, (const float*)M, rows, cols, ld, x,
+                          alpha, out, mode, vec));
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;
 }
@@ -143,18 +149,21 @@ int woodbury_apply(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t
   char* b = (char*)wsp;
   double *y = (double*)b, *w = (double*)(b + off_w), *t = (double*)(b + off_t);
   double *u = (double*)(b + off_u), *part = (double*)(b + off_p);
-  k_div_vec<<<(unsigned)cdiv(d, 256), 256, 0, st>>>(z, lam, d, y);
+  ADASK_CUDA(launch_pdl(k_div_vec, dim3((unsigned)cdiv(d, 256)), dim3(256), 0, st, z, lam, d, y));
   ADASK_LAUNCHED(ctx);
   ADASK_TRY(gemv_rows(ctx, dtype, SA, m, d, ldsa, y, 1.0, w, 0, st));     // w = SA y
   ADASK_TRY(gemv_rows(ctx, dtype, Linv, m, m, ldl, w, 1.0, t, 1, st));    // t = L^-1 w
   ADASK_TRY(gemv_rows(ctx, dtype, LinvT, m, m, ldl, t, 1.0, u, 2, st));   // u = L^-T t
   dim3 g((unsigned)cdiv(d, 256), (unsigned)nb);
   if (dtype == ADASK_F64)
-    k_gemv_cols<double><<<g, 256, 0, st>>>((const double*)SA, m, d, ldsa, u, part);
+    ADASK_CUDA(launch_pdl(k_gemv_cols<double>, g, dim3(256), 0, st, (const double*)SA, m, d, ldsa, (const double*)u,
+                          part));
   else
-    k_gemv_cols<float><<<g, 256, 0, st>>>((const float*)SA, m, d, ldsa, u, part);
+    ADASK_CUDA(launch_pdl(k_gemv_cols<float>, g, dim3(256), 0, st, (const float*)SA, m, d, ldsa, (const double*)u,
+                          part));
   ADASK_LAUNCHED(ctx);
-  k_woodbury_finish<<<(unsigned)cdiv(d, 256), 256, 0, st>>>(part, nb, d, y, lam, nu2, out);
+  ADASK_CUDA(launch_pdl(k_woodbury_finish, dim3((unsigned)cdiv(d, 256)), dim3(256), 0, st, (const double*)part, nb,
+                        d, (const double*)y, lam, nu2, out));
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;
 }

@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(1024) k_hess_finish(const double* __restrict__
                                                       const double* __restrict__ lam,
                                                       const double* __restrict__ B, double* __restrict__ out,
                                                       int epilogue) {
+  pdl_wait();
   // 32 columns x 32 partial groups; each thread sums its parts with four
   // independent accumulators (all loads in flight at once), then group 0
   // combines the 32 group sums -- a fixed order, so the result is deterministic
@@ -440,6 +441,7 @@ __global__ void __launch_bounds__(1024) k_hess_finish_pair(const double* __restr
                                                            const double* __restrict__ B0,
                                                            const double* __restrict__ B1, double* __restrict__ out0,
                                                            double* __restrict__ out1, int epilogue) {
+  pdl_wait();
   const bool q = blockIdx.y != 0;
   const double* part = q ? part1 : part0;
   const double* x = q ? x1 : x0;
@@ -628,9 +630,9 @@ int hess_mult_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t 
     } else {
       return fail(ADASK_E_ARG, "bad dtype %d", dtype);
     }
-    k_hess_finish<<<(unsigned)cdiv(d, 32), 1024, 0, st>>>(part, nparts, d, x, nu2, lam,
-                                                         B ? B + j * ldb : nullptr,
-                                                         out + j * ldo, partial ? 0 : 1);
+    ADASK_CUDA(launch_pdl(k_hess_finish, dim3((unsigned)cdiv(d, 32)), dim3(1024), 0, st, (const double*)part, nparts,
+                          d, x, nu2, lam, B ? B + j * ldb : (const double*)nullptr, out + j * ldo,
+                          partial ? 0 : 1));
     ADASK_LAUNCHED(ctx);
   }
   return ADASK_OK;
@@ -653,8 +655,8 @@ int hess_mult_pair_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int
   else
     ADASK_TRY(hess_partial_tma<float>(ctx, (const float*)A, n, d, lda, x0, &part0, &nparts, st, &used, x1, &part1));
   if (!used) return ADASK_OK;
-  k_hess_finish_pair<<<dim3((unsigned)cdiv(d, 32), 2), 1024, 0, st>>>(part0, part1, nparts, d, x0, x1, nu2, lam,
-                                                                       B0, B1, out0, out1, partial ? 0 : 1);
+  ADASK_CUDA(launch_pdl(k_hess_finish_pair, dim3((unsigned)cdiv(d, 32), 2), dim3(1024), 0, st, (const double*)part0,
+                        (const double*)part1, nparts, d, x0, x1, nu2, lam, B0, B1, out0, out1, partial ? 0 : 1));
   ADASK_LAUNCHED(ctx);
   *fused = 1;
   return ADASK_OK;

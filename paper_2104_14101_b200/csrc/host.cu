@@ -386,6 +386,10 @@ int64_t adask_ctx_launches(const adask_ctx* ctx) { return ctx ? ctx->launches : 
 }  // extern "C"
 
 namespace adask {
+bool pdl_enabled() {
+  static const bool on = getenv("ADASK_NO_PDL") == nullptr;
+  return on;
+}
 int ensure_smem_attr(const void* fn, int bytes) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> done;

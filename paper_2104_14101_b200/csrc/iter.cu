@@ -32,6 +32,7 @@ __device__ __forceinline__ double blk_sum(double v, double* sh) { return block_s
 __global__ void __launch_bounds__(kVecThreads) k_pcg_restart_tail(int64_t d, int64_t c, const double* rt,
                                                                   double* r, double* p, double* dt_col,
                                                                   IterScalars* sc) {
+  pdl_wait();
   __shared__ double sh[32];
   double tot = 0.0;
   int flags = 0;
@@ -58,6 +59,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pcg_restart_tail(int64_t d, int
 }
 
 __global__ void k_negate(double* v, int64_t n) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = -v[i];
 }
@@ -68,6 +70,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pcg_step(int64_t d, int64_t c, 
                                                           const double* Hp, const double* dt_col,
                                                           double* x_new, double* r_new,
                                                           IterScalars* sc) {
+  pdl_wait();
   __shared__ double sh[32];
   int flags = 0;
   for (int64_t j = 0; j < c; ++j) {
@@ -89,6 +92,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pcg_step(int64_t d, int64_t c, 
 __global__ void __launch_bounds__(kVecThreads) k_pcg_scalars(int64_t d, int64_t c, const double* r,
                                                              const double* rt, double* dt_new,
                                                              IterScalars* sc) {
+  pdl_wait();
   __shared__ double sh[32];
   double tot = 0.0;
   int flags = 0;
@@ -115,6 +119,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pcg_scalars(int64_t d, int64_t 
 // commit: p = rt_new + p * ratio,  ratio = old > 0 ? dt_new / old : 0  (solvers.py:277-282)
 __global__ void k_pcg_commit(int64_t d, int64_t c, const double* rt_new, const double* dt_new,
                              const double* dt_old, double* p) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d * c) return;
   const int64_t j = i / d;
@@ -127,6 +132,7 @@ __global__ void k_pcg_commit(int64_t d, int64_t c, const double* rt_new, const d
 __global__ void __launch_bounds__(kVecThreads) k_half_dot(int64_t d, int64_t c, int64_t ld,
                                                           const double* a, const double* b,
                                                           IterScalars* sc) {
+  pdl_wait();
   __shared__ double sh[32];
   double tot = 0.0;
   for (int64_t j = 0; j < c; ++j) {
@@ -143,6 +149,7 @@ __global__ void __launch_bounds__(kVecThreads) k_half_dot(int64_t d, int64_t c, 
 // IHS / heavy-ball step: x_new = x - mu v (+ beta (x - x_prev))   (solvers.py:538, 562)
 __global__ void k_ihs_step(int64_t n, const double* x, const double* v, double mu,
                            const double* x_prev, double beta, double* x_new) {
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double t = x[i] - mu * v[i];
@@ -189,6 +196,7 @@ static int check_problem(const adask_problem* pb) {
 }
 
 __global__ void k_negate_copy(const double* __restrict__ a, double* __restrict__ out, int64_t n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = -a[i];
 }
@@ -225,11 +233,13 @@ int pcg_propose_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precon
   if (!*hx_ok) ADASK_TRY(problem_hess(ctx, pb, p, nullptr, Hp, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  k_pcg_step<<<1, kVecThreads, 0, st>>>(d, c, x, r, p, Hp, dt_col, x_new, r_new, sc);
-  ADASK_LAUNCHED(ctx);
+  ADASK_CUDA(launch_pdl(k_pcg_step, dim3(1), dim3(kVecThreads), 0, st, d, c, x, r, p, (const double*)Hp, dt_col,
+                        x_new, r_new, sc));
+  ctx->launches++;
   ADASK_TRY(precond_apply_impl(ctx, P, r_new, c, d, rt_new, d, st));
-  k_pcg_scalars<<<1, kVecThreads, 0, st>>>(d, c, r_new, rt_new, dt_new, sc);
-  ADASK_LAUNCHED(ctx);
+  ADASK_CUDA(launch_pdl(k_pcg_scalars, dim3(1), dim3(kVecThreads), 0, st, d, c, (const double*)r_new,
+                        (const double*)rt_new, dt_new, sc));
+  ctx->launches++;
   int flags = 0;
   ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
   if (flags & FLAG_BREAKDOWN) return fail(ADASK_E_BREAKDOWN, "direction with nonpositive curvature");
@@ -244,18 +254,18 @@ int pcg_restart_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precon
   ADASK_TRY(check_problem(pb));
   const int64_t d = pb->d, c = pb->c;
   if (hx_mb) {
-    k_negate_copy<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(hx_mb, r, d * c);
+    ADASK_CUDA(launch_pdl(k_negate_copy, dim3((unsigned)cdiv(d * c, 256)), dim3(256), 0, st, hx_mb, r, d * c));
     ADASK_LAUNCHED(ctx);
   } else {
     // r = B - H x   (computed as -(H x - B), exact)
     ADASK_TRY(problem_hess(ctx, pb, x, pb->B, r, st));
-    k_negate<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(r, d * c);
+    ADASK_CUDA(launch_pdl(k_negate, dim3((unsigned)cdiv(d * c, 256)), dim3(256), 0, st, r, d * c));
     ADASK_LAUNCHED(ctx);
   }
   ADASK_TRY(precond_apply_impl(ctx, P, r, c, d, rt, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  k_pcg_restart_tail<<<1, kVecThreads, 0, st>>>(d, c, rt, r, p, dt_col, sc);
+  ADASK_CUDA(launch_pdl(k_pcg_restart_tail, dim3(1), dim3(kVecThreads), 0, st, d, c, rt, r, p, dt_col, sc));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
@@ -275,7 +285,7 @@ int ihs_restart_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precon
   ADASK_TRY(precond_apply_impl(ctx, P, g, c, d, v, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  k_half_dot<<<1, kVecThreads, 0, st>>>(d, c, d, g, v, sc);
+  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g, v, sc));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
@@ -294,12 +304,12 @@ extern "C" int adask_pcg_restart(adask_ctx* ctx, const adask_problem* pb, const 
   const int64_t d = pb->d, c = pb->c;
   // r = B - H x   (computed as -(H x - B), exact)
   ADASK_TRY(problem_hess(ctx, pb, x, pb->B, r, st));
-  k_negate<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(r, d * c);
+  ADASK_CUDA(launch_pdl(k_negate, dim3((unsigned)cdiv(d * c, 256)), dim3(256), 0, st, r, d * c));
   ADASK_LAUNCHED(ctx);
   ADASK_TRY(precond_apply_impl(ctx, P, r, c, d, rt, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  k_pcg_restart_tail<<<1, kVecThreads, 0, st>>>(d, c, rt, r, p, dt_col, sc);
+  ADASK_CUDA(launch_pdl(k_pcg_restart_tail, dim3(1), dim3(kVecThreads), 0, st, d, c, rt, r, p, dt_col, sc));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
@@ -335,7 +345,7 @@ extern "C" int adask_pcg_commit(adask_ctx* ctx, int64_t d, int64_t c, const doub
                                 const double* dt_new, const double* dt_old, double* p, void* stream) {
   ADASK_TRY(use_device(ctx));
   cudaStream_t st = S(stream);
-  k_pcg_commit<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(d, c, rt_new, dt_new, dt_old, p);
+  ADASK_CUDA(launch_pdl(k_pcg_commit, dim3((unsigned)cdiv(d * c, 256)), dim3(256), 0, st, d, c, rt_new, dt_new, dt_old, p));
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;
 }
@@ -351,7 +361,7 @@ extern "C" int adask_ihs_restart(adask_ctx* ctx, const adask_problem* pb, const 
   ADASK_TRY(precond_apply_impl(ctx, P, g, c, d, v, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  k_half_dot<<<1, kVecThreads, 0, st>>>(d, c, d, g, v, sc);
+  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g, v, sc));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
@@ -365,13 +375,13 @@ extern "C" int adask_ihs_propose(adask_ctx* ctx, const adask_problem* pb, const 
   ADASK_TRY(check_problem(pb));
   cudaStream_t st = S(stream);
   const int64_t d = pb->d, c = pb->c;
-  k_ihs_step<<<(unsigned)cdiv(d * c, 256), 256, 0, st>>>(d * c, x, v, mu, x_prev, beta, x_new);
+  ADASK_CUDA(launch_pdl(k_ihs_step, dim3((unsigned)cdiv(d * c, 256)), dim3(256), 0, st, d * c, x, v, mu, x_prev, beta, x_new));
   ADASK_LAUNCHED(ctx);
   ADASK_TRY(problem_hess(ctx, pb, x_new, pb->B, g_new, st));
   ADASK_TRY(precond_apply_impl(ctx, P, g_new, c, d, v_new, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  k_half_dot<<<1, kVecThreads, 0, st>>>(d, c, d, g_new, v_new, sc);
+  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g_new, v_new, sc));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
@@ -383,7 +393,7 @@ extern "C" int adask_dot(adask_ctx* ctx, const double* a, const double* b, int64
   cudaStream_t st = S(stream);
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  k_half_dot<<<1, kVecThreads, 0, st>>>(d, c, ld, a, b, sc);
+  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, ld, a, b, sc));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   return read_scalars(ctx, sc, result_host, &flags, st);
