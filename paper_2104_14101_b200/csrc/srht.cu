@@ -282,6 +282,29 @@ static int dispatch_fw(adask_ctx* ctx, int log, const FwhtArgs& a, int64_t nblk,
   }
 }
 
+// Pass 2 of the tile kernels over a Z written by the pipelined pass 1
+// (srht_pipe.cu, same slot numbering and layout Z[(slot*G + blk)*d + col]):
+// the hybrid used for fp64 with many selected rows, where the tile kernels'
+// short (2^(L-10)-point) transforms beat the pipelined pass 2.
+int fwht_tile_pass2(adask_ctx* ctx, int dtype, int L2, const void* Z, int64_t G, int64_t d, int64_t nslots,
+                    const int32_t* d_slot_start, const int32_t* d_ent_hi, const int32_t* d_ent_k, void* out,
+                    int64_t ldo, double c1, double c2, int accumulate, cudaStream_t st) {
+  FwhtArgs a{};
+  a.Z = const_cast<void*>(Z);
+  a.G = G;
+  a.d = d;
+  a.slot_start = d_slot_start;
+  a.ent_hi = d_ent_hi;
+  a.ent_k = d_ent_k;
+  a.out = out;
+  a.ldo = ldo;
+  a.c1 = c1;
+  a.c2 = c2;
+  a.accumulate = accumulate;
+  if (dtype == ADASK_F64) return dispatch_fw<double, FW_P2>(ctx, L2, a, nslots, st);
+  return dispatch_fw<float, FW_P2>(ctx, L2, a, nslots, st);
+}
+
 static int ilog2(int64_t n) {
   int l = 0;
   while ((1ll << l) < n) ++l;
@@ -296,8 +319,9 @@ static int fwht_select(adask_ctx* ctx, int dtype, const void* A, int64_t n, int6
                        void* out, int64_t ldo, double c1, double c2, int accumulate,
                        cudaStream_t st) {
   // 2^12..2^22 padded rows: persistent TMA-pipelined passes (srht_pipe.cu)
-  if (fwht_pipe_eligible(dtype, A, n, n_pad, lda, m, idx != nullptr))
-    return fwht_select_pipe(ctx, dtype, A, n, d, lda, sgn, n_pad, idx, m, out, ldo, c1, c2, accumulate, st);
+  if (const int pe = fwht_pipe_eligible(dtype, A, n, n_pad, lda, m, idx != nullptr))
+    return fwht_select_pipe(ctx, dtype, A, n, d, lda, sgn, n_pad, idx, m, out, ldo, c1, c2, accumulate, st,
+                            pe == 2);
   const int L = ilog2(n_pad);
   int b1 = std::max(std::min(L, 10), L - 12);
   // many slots (m >= 4096 of >= 2^20 rows): the 11-bit pass-1 tiles and the

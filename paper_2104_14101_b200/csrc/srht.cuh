@@ -16,6 +16,9 @@ int srht_gather_impl(adask_ctx* ctx, int dtype, const void* Y, int64_t n_pad, in
 int fwht_pipe_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int64_t lda, int64_t m, bool selected);
 int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                      const uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out, int64_t ldo,
-                     double c1, double c2, int accumulate, cudaStream_t st);
+                     double c1, double c2, int accumulate, cudaStream_t st, int hybrid = 0);
+int fwht_tile_pass2(adask_ctx* ctx, int dtype, int L2, const void* Z, int64_t G, int64_t d, int64_t nslots,
+                    const int32_t* d_slot_start, const int32_t* d_ent_hi, const int32_t* d_ent_k, void* out,
+                    int64_t ldo, double c1, double c2, int accumulate, cudaStream_t st);
 int fwht_build_map2(adask_ctx* ctx, const int32_t* pos, int64_t m, int32_t* map2, int64_t rows, cudaStream_t st);
 }  // namespace adask

@@ -620,9 +620,11 @@ static int ilog2p(int64_t n) {
 
 // 0 = not eligible (caller uses the tile kernels), 1 = eligible.
 int fwht_pipe_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int64_t lda, int64_t m, bool selected) {
+  int force = -1;
   if (const char* e = getenv("ADASK_FWHT_PIPE")) {
     if (atoi(e) == 0) return 0;
-    if (atoi(e) == 2) m = 0;  // force (tests)
+    if (atoi(e) == 2) m = 0;      // force the pipelined passes (tests)
+    if (atoi(e) == 3) force = 2;  // force the hybrid (tests)
   }
   const int L = ilog2p(n_pad);
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
@@ -631,14 +633,16 @@ int fwht_pipe_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int64
   if (((uintptr_t)A & 15) || ((size_t)lda * esz) % 16) return 0;
   if (n % 32) return 0;  // the [e][q] tensor-map view of A needs whole 32-row groups
   // fp64 with many selected rows: the tile kernels' pass 2 is faster on the
-  // short (2^(L-10)-point) transforms (measured at 2^16 x 1024, m = 1024-4096)
-  if (dtype == ADASK_F64 && m > 512) return 0;
+  // short (2^(L-10)-point) transforms (measured at 2^16 x 1024, m = 1024-4096):
+  // pipelined pass 1 + tile pass 2 (2), or all tile kernels (0) past 2^20 rows
+  if (force == 2) return (selected && L <= 20) ? 2 : 0;
+  if (dtype == ADASK_F64 && m >= 512) return (selected && L <= 20) ? 2 : 0;
   return 1;
 }
 
 int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                      const uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out, int64_t ldo,
-                     double c1, double c2, int accumulate, cudaStream_t st) {
+                     double c1, double c2, int accumulate, cudaStream_t st, int hybrid) {
   const int L = ilog2p(n_pad);
   const int b1 = 10;  // pass-1 tiles are 2^10-row blocks
   const int L2 = L - b1;
@@ -675,14 +679,37 @@ int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   int32_t* d_plan = nullptr;
   int32_t* d_map2 = nullptr;
   int32_t* d_rep = nullptr;
+  const int64_t ldz_h = (int64_t)align_up((size_t)d, 16 / esz);
+  hybrid = hybrid && idx && !comb && ldz_h == d;
+  std::vector<int32_t> old_plan;  // hybrid: slot_start [nslots + 1] | ent_hi [m] | ent_k [m]
+  if (hybrid) {
+    old_plan.assign((size_t)(nslots + 1 + 2 * m), 0);
+    int32_t* ss = old_plan.data();
+    int32_t* eh = ss + nslots + 1;
+    int32_t* ek = eh + m;
+    for (int64_t k = 0; k < m; ++k) ss[plan[(size_t)(idx[k] & (B - 1))] + 1]++;
+    for (int64_t q = 0; q < nslots; ++q) ss[q + 1] += ss[q];
+    std::vector<int32_t> fill(ss, ss + nslots);
+    for (int64_t k = 0; k < m; ++k) {
+      const int32_t q = plan[(size_t)(idx[k] & (B - 1))];
+      const int32_t pos = fill[(size_t)q]++;
+      eh[pos] = (int32_t)(idx[k] >> b1);
+      ek[pos] = (int32_t)k;
+    }
+  }
   if (idx) {
     void* pw = nullptr;
-    ADASK_TRY(ctx->ws[WS_PLAN].get((plan.size() + (size_t)map_rows + (size_t)m) * 4 + 128, st, &pw));
+    ADASK_TRY(ctx->ws[WS_PLAN].get((plan.size() + (size_t)map_rows + (size_t)m + old_plan.size()) * 4 + 256, st,
+                                   &pw));
     d_plan = (int32_t*)pw;
     d_map2 = d_plan + align_up(plan.size(), 16);
     d_rep = d_map2 + align_up((size_t)map_rows, 16);
     ADASK_CUDA(cudaMemcpyAsync(d_plan, plan.data(), plan.size() * 4, cudaMemcpyHostToDevice, st));
-    if (comb)
+    if (hybrid) {
+      int32_t* d_old = d_rep + align_up((size_t)m, 16);
+      ADASK_CUDA(cudaMemcpyAsync(d_old, old_plan.data(), old_plan.size() * 4, cudaMemcpyHostToDevice, st));
+      d_map2 = d_old;  // reused below as the old plan's base
+    } else if (comb)
       ADASK_TRY(fwht_build_map2_comb(ctx, d_plan + B, m, d_map2, map_rows, d_rep, st));
     else
       ADASK_TRY(fwht_build_map2(ctx, d_plan + B, m, d_map2, map_rows, st));
@@ -714,6 +741,16 @@ int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   a.accumulate = comb ? 0 : accumulate;
   a.vec_out = ((uintptr_t)a.out % 16 == 0) && ((size_t)a.ldo * esz) % 16 == 0;
   // pass 1 reads rows [0, n) of A; rows [n, n_pad) are TMA out-of-bounds zeros
+  if (hybrid) {
+    a.map2 = nullptr;
+    if (dtype == ADASK_F64)
+      ADASK_TRY((dispatch_pipe<double, P1>(ctx, dtype, b1, A, n, n_pad, lda, a, st)));
+    else
+      ADASK_TRY((dispatch_pipe<float, P1>(ctx, dtype, b1, A, n, n_pad, lda, a, st)));
+    const int32_t* ss = d_map2;
+    return fwht_tile_pass2(ctx, dtype, L2, zw, G, d, nslots, ss, ss + nslots + 1, ss + nslots + 1 + m, out, ldo, c1,
+                           c2, accumulate, st);
+  }
   if (dtype == ADASK_F64) {
     ADASK_TRY((dispatch_pipe<double, P1>(ctx, dtype, b1, A, n, n_pad, lda, a, st)));
     ADASK_TRY((dispatch_pipe<double, P2>(ctx, dtype, L2p, zw, zrows, zrows, ldz, a, st)));

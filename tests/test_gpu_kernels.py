@@ -126,6 +126,17 @@ def test_srht_pipelined_passes_bitwise(ak, n, d, m, seed, monkeypatch):
     assert np.array_equal(got, O.sketch_srht(A, m, seed))
 
 
+@pytest.mark.parametrize("n,d,m,seed", [(1 << 16, 40, 4096, 1), (1 << 14, 20, 1 << 14, 2), (4096, 24, 1000, 3),
+                                        ((1 << 17) + 32, 16, 2000, 4), (1 << 20, 6, 600, 5)])
+def test_srht_hybrid_passes_bitwise(ak, n, d, m, seed, monkeypatch):
+    """Pipelined pass 1 + tile-kernel pass 2 (the fp64 many-row default,
+    forced with ADASK_FWHT_PIPE=3) reproduces the reference SRHT bit for bit."""
+    monkeypatch.setenv("ADASK_FWHT_PIPE", "3")
+    A = np.random.default_rng(seed).standard_normal((n, d))
+    got = ak.sketch_srht(A, m, seed).SA
+    assert np.array_equal(got, O.sketch_srht(A, m, seed))
+
+
 @pytest.mark.parametrize("n,d,m", [(1 << 16, 64, 64), (1 << 16, 48, 4096), ((1 << 21) - 64, 16, 32768),
                                    (1 << 21, 20, 100)])
 def test_srht_pipelined_fp32_matches_tile_kernels(ak, n, d, m, monkeypatch):
