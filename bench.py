@@ -44,9 +44,11 @@ def _peaks() -> dict:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
         return {"hbm_gbs": float(pk["hbm_gbs"]), "bf16_tflops": float(pk["bf16_tflops"]),
+                "bf16_tflops_sustained": float(pk.get("bf16_tflops_sustained", pk["bf16_tflops"])),
                 "source": "MEASURED_PEAKS.json (measured)"}
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "B200_PROFILING.md fallback"}
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "B200_PROFILING.md fallback"}
 
 
 class ClockSampler:
@@ -406,7 +408,9 @@ def run_ours(args) -> None:
     if tensor:  # TF32 tcgen05 GEMM: tensor-bound; peak = half the measured dense bf16 rate
         work_per = u["flops"] / max(u["count"], 1)
         achieved = work_per / (per_launch_ms * 1e-3) / 1e12
-        peak, unit, bound = pk["bf16_tflops"] / 2.0, "TFLOP/s", "tensor"
+        # the sketch runs inside a long solve under the power cap: the sustained
+        # bf16 figure (B200_PROFILING.md), halved for TF32 (dense TF32 = bf16 / 2)
+        peak, unit, bound = pk["bf16_tflops_sustained"] / 2.0, "TFLOP/s", "tensor"
     else:
         work_per = u["bytes"] / max(u["count"], 1)
         achieved = work_per / (per_launch_ms * 1e-3) / 1e9
@@ -462,7 +466,8 @@ def run_ours(args) -> None:
             "roofline": {"bound": bound, "unit_name": dom, "achieved": achieved, "peak": peak,
                          "unit": unit, "frac": achieved / peak, "traffic": traffic,
                          "per_launch_ms": per_launch_ms, "alg_work_per_launch": work_per,
-                         "peak_source": pk["source"] + (" (bf16/2 for tf32)" if tensor else "")},
+                         "peak_source": pk["source"] + (" (sustained bf16 / 2 for tf32: the sketch runs inside a "
+                                                        "long solve under the power cap)" if tensor else "")},
             "clocks": clk.summary(),
             "e2e": e2e,
             "incremental": incr,
