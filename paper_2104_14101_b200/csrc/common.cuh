@@ -129,6 +129,14 @@ struct adask_ctx {
   // native driver: the Cholesky's pivot check is read at the driver's next
   // stream synchronization instead of a sync of its own (pinned_flags[1])
   bool defer_spd = false;
+  // pinned staging ring for host -> device plan uploads (adask::upload_async)
+  struct Stage {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  } stage[4];
+  int stage_next = 0;
 };
 
 namespace adask {
@@ -158,6 +166,11 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, (KArgs)args...);
 }
+// Host -> device copy through a ring of pinned staging buffers: stream
+// ordered and asynchronous (a cudaMemcpyAsync from pageable memory first
+// synchronizes the stream, so the host could not prepare the next block's
+// plan while the GPU works on this one).
+int upload_async(adask_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
 // the driver call costs microseconds of host time, and on the per-iteration
 // path the GPU idles while the host issues the next kernel.

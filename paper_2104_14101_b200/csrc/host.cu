@@ -377,6 +377,13 @@ int adask_ctx_destroy(adask_ctx* ctx) {
   adask::blas_release(ctx);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
+  for (auto& b : ctx->stage) {
+    if (b.ev) {
+      cudaEventSynchronize(b.ev);
+      cudaEventDestroy(b.ev);
+    }
+    if (b.p) cudaFreeHost(b.p);
+  }
   delete ctx;
   return ADASK_OK;
 }
@@ -386,6 +393,30 @@ int64_t adask_ctx_launches(const adask_ctx* ctx) { return ctx ? ctx->launches : 
 }  // extern "C"
 
 namespace adask {
+int upload_async(adask_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return ADASK_OK;
+  adask_ctx::Stage& b = ctx->stage[ctx->stage_next];
+  ctx->stage_next = (ctx->stage_next + 1) % 4;
+  if (b.pending) {
+    ADASK_CUDA(cudaEventSynchronize(b.ev));  // its previous copy has been consumed
+    b.pending = false;
+  }
+  if (b.bytes < bytes) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    const size_t nb = std::max<size_t>(bytes + bytes / 4, 64 * 1024);
+    ADASK_CUDA(cudaMallocHost(&b.p, nb));
+    b.bytes = nb;
+  }
+  if (!b.ev) ADASK_CUDA(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+  memcpy(b.p, src, bytes);
+  ADASK_CUDA(cudaMemcpyAsync(dst, b.p, bytes, cudaMemcpyHostToDevice, st));
+  ADASK_CUDA(cudaEventRecord(b.ev, st));
+  b.pending = true;
+  return ADASK_OK;
+}
+
 bool pdl_enabled() {
   static const bool on = getenv("ADASK_NO_PDL") == nullptr;
   return on;

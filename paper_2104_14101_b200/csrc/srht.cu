@@ -377,7 +377,7 @@ static int fwht_select(adask_ctx* ctx, int dtype, const void* A, int64_t n, int6
   plan.insert(plan.end(), ent_k.begin(), ent_k.end());
   void* pw = nullptr;
   ADASK_TRY(ctx->ws[WS_PLAN].get(plan.size() * 4, st, &pw));
-  ADASK_CUDA(cudaMemcpyAsync(pw, plan.data(), plan.size() * 4, cudaMemcpyHostToDevice, st));
+  ADASK_TRY(upload_async(ctx, pw, plan.data(), plan.size() * 4, st));
   const int32_t* d_lo = (const int32_t*)pw;
   const int32_t* d_ss = d_lo + B;
   const int32_t* d_hi = d_ss + nslots + 1;

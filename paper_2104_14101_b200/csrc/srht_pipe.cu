@@ -704,10 +704,10 @@ int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
     d_plan = (int32_t*)pw;
     d_map2 = d_plan + align_up(plan.size(), 16);
     d_rep = d_map2 + align_up((size_t)map_rows, 16);
-    ADASK_CUDA(cudaMemcpyAsync(d_plan, plan.data(), plan.size() * 4, cudaMemcpyHostToDevice, st));
+    ADASK_TRY(upload_async(ctx, d_plan, plan.data(), plan.size() * 4, st));
     if (hybrid) {
       int32_t* d_old = d_rep + align_up((size_t)m, 16);
-      ADASK_CUDA(cudaMemcpyAsync(d_old, old_plan.data(), old_plan.size() * 4, cudaMemcpyHostToDevice, st));
+      ADASK_TRY(upload_async(ctx, d_old, old_plan.data(), old_plan.size() * 4, st));
       d_map2 = d_old;  // reused below as the old plan's base
     } else if (comb)
       ADASK_TRY(fwht_build_map2_comb(ctx, d_plan + B, m, d_map2, map_rows, d_rep, st));
