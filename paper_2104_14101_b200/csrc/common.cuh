@@ -137,6 +137,11 @@ struct adask_ctx {
     bool pending = false;
   } stage[4];
   int stage_next = 0;
+  // host-mapped mailbox of the iteration decrements: the last kernel of each
+  // body writes delta_tilde / flags / a sequence number into pinned memory,
+  // the host spins on the sequence number (no copy-engine D2H, no stream sync)
+  void* mail = nullptr;
+  uint32_t mail_seq = 0;
 };
 
 namespace adask {

@@ -377,6 +377,7 @@ int adask_ctx_destroy(adask_ctx* ctx) {
   adask::blas_release(ctx);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
+  if (ctx->mail) cudaFreeHost(ctx->mail);
   for (auto& b : ctx->stage) {
     if (b.ev) {
       cudaEventSynchronize(b.ev);

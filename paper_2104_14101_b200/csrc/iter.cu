@@ -7,6 +7,10 @@
 // decrement plus guard flags -- the single host synchronisation the adaptive
 // accept/reject rule needs per loop pass.  All reductions are fixed-order
 // (bitwise reproducible).
+#include <atomic>
+#include <chrono>
+#include <cstring>
+
 #include "common.cuh"
 #include "hessmult.cuh"
 #include "precond.cuh"
@@ -22,6 +26,21 @@ struct IterScalars {
   int pad2[7];
 };
 
+struct IterMail {
+  double delta_tilde;
+  int flags;
+  uint32_t seq;
+};
+
+// thread 0, after writing sc: the host-visible copy, then the sequence number
+__device__ __forceinline__ void publish(const IterScalars* sc, IterMail* mail, uint32_t seq) {
+  if (!mail) return;
+  mail->delta_tilde = sc->delta_tilde;
+  mail->flags = sc->flags;
+  __threadfence_system();
+  *reinterpret_cast<volatile uint32_t*>(&mail->seq) = seq;
+}
+
 constexpr int kVecThreads = 1024;
 
 // Fixed-order block sum (kVecThreads threads).
@@ -31,7 +50,7 @@ __device__ __forceinline__ double blk_sum(double v, double* sh) { return block_s
 // with the NegativeValue guard (solvers.py:245-255).
 __global__ void __launch_bounds__(kVecThreads) k_pcg_restart_tail(int64_t d, int64_t c, const double* rt,
                                                                   double* r, double* p, double* dt_col,
-                                                                  IterScalars* sc) {
+                                                                  IterScalars* sc, IterMail* mail, uint32_t seq) {
   pdl_wait();
   __shared__ double sh[32];
   double tot = 0.0;
@@ -55,6 +74,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pcg_restart_tail(int64_t d, int
   if (threadIdx.x == 0) {
     sc->delta_tilde = 0.5 * tot;
     sc->flags = flags;
+    publish(sc, mail, seq);
   }
 }
 
@@ -91,7 +111,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pcg_step(int64_t d, int64_t c, 
 // PCG propose, second half: dt_new = _scalars(r_new, rt_new)
 __global__ void __launch_bounds__(kVecThreads) k_pcg_scalars(int64_t d, int64_t c, const double* r,
                                                              const double* rt, double* dt_new,
-                                                             IterScalars* sc) {
+                                                             IterScalars* sc, IterMail* mail, uint32_t seq) {
   pdl_wait();
   __shared__ double sh[32];
   double tot = 0.0;
@@ -113,6 +133,7 @@ __global__ void __launch_bounds__(kVecThreads) k_pcg_scalars(int64_t d, int64_t 
   if (threadIdx.x == 0) {
     sc->delta_tilde = 0.5 * tot;
     sc->flags |= flags;
+    publish(sc, mail, seq);
   }
 }
 
@@ -131,7 +152,7 @@ __global__ void k_pcg_commit(int64_t d, int64_t c, const double* rt_new, const d
 // 0.5 * sum(a .* b)
 __global__ void __launch_bounds__(kVecThreads) k_half_dot(int64_t d, int64_t c, int64_t ld,
                                                           const double* a, const double* b,
-                                                          IterScalars* sc) {
+                                                          IterScalars* sc, IterMail* mail, uint32_t seq) {
   pdl_wait();
   __shared__ double sh[32];
   double tot = 0.0;
@@ -143,6 +164,7 @@ __global__ void __launch_bounds__(kVecThreads) k_half_dot(int64_t d, int64_t c, 
   if (threadIdx.x == 0) {
     sc->delta_tilde = 0.5 * tot;
     sc->flags = 0;
+    publish(sc, mail, seq);
   }
 }
 
@@ -161,11 +183,48 @@ static int get_scalars(adask_ctx* ctx, IterScalars** sc, cudaStream_t st) {
   void* wsp = nullptr;
   ADASK_TRY(ctx->ws[WS_SMALL].get(sizeof(IterScalars), st, &wsp));
   *sc = (IterScalars*)wsp;
+  if (!ctx->mail && !getenv("ADASK_NO_MAILBOX")) {
+    void* mp = nullptr;
+    if (cudaMallocHost(&mp, sizeof(IterMail) + 64) == cudaSuccess) {
+      memset(mp, 0, sizeof(IterMail) + 64);
+      ctx->mail = mp;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  ++ctx->mail_seq;
+  if (ctx->mail_seq == 0) ctx->mail_seq = 1;
   return ADASK_OK;
 }
 
+static IterMail* mail_of(adask_ctx* ctx) { return reinterpret_cast<IterMail*>(ctx->mail); }
+
+// The decrement and guard flags of the body just enqueued: from the mailbox
+// (spin on its sequence number; errors surface through a stream query every
+// ~50 ms of waiting), or, without one, a D2H copy and a stream sync.
 static int read_scalars(adask_ctx* ctx, IterScalars* sc, double* dt_host, int* flags,
                         cudaStream_t st) {
+  IterMail* m = mail_of(ctx);
+  if (m) {
+    const uint32_t want = ctx->mail_seq;
+    volatile uint32_t* seq = &m->seq;
+    auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t spin = 0; *seq != want; ++spin) {
+      if ((spin & 0xFFFF) == 0xFFFF) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q != cudaSuccess && q != cudaErrorNotReady)
+          return fail(ADASK_E_CUDA, "iteration body failed: %s", cudaGetErrorString(q));
+        if (q == cudaSuccess && *seq != want)
+          return fail(ADASK_E_CUDA, "iteration mailbox not written (sequence %u)", want);
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(600))
+          return fail(ADASK_E_CUDA, "iteration mailbox wait timed out");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (dt_host) *dt_host = ((volatile IterMail*)m)->delta_tilde;
+    *flags = ((volatile IterMail*)m)->flags;
+    return ADASK_OK;
+  }
   ADASK_CUDA(cudaMemcpyAsync(ctx->pinned, sc, sizeof(IterScalars), cudaMemcpyDeviceToHost, st));
   ADASK_CUDA(cudaStreamSynchronize(st));
   const IterScalars* h = reinterpret_cast<const IterScalars*>(ctx->pinned);
@@ -238,7 +297,7 @@ int pcg_propose_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precon
   ctx->launches++;
   ADASK_TRY(precond_apply_impl(ctx, P, r_new, c, d, rt_new, d, st));
   ADASK_CUDA(launch_pdl(k_pcg_scalars, dim3(1), dim3(kVecThreads), 0, st, d, c, (const double*)r_new,
-                        (const double*)rt_new, dt_new, sc));
+                        (const double*)rt_new, dt_new, sc, mail_of(ctx), ctx->mail_seq));
   ctx->launches++;
   int flags = 0;
   ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
@@ -265,7 +324,8 @@ int pcg_restart_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precon
   ADASK_TRY(precond_apply_impl(ctx, P, r, c, d, rt, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  ADASK_CUDA(launch_pdl(k_pcg_restart_tail, dim3(1), dim3(kVecThreads), 0, st, d, c, rt, r, p, dt_col, sc));
+  ADASK_CUDA(launch_pdl(k_pcg_restart_tail, dim3(1), dim3(kVecThreads), 0, st, d, c, rt, r, p, dt_col, sc,
+                        mail_of(ctx), ctx->mail_seq));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
@@ -285,7 +345,8 @@ int ihs_restart_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precon
   ADASK_TRY(precond_apply_impl(ctx, P, g, c, d, v, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g, v, sc));
+  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g, v, sc, mail_of(ctx),
+                        ctx->mail_seq));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
@@ -309,7 +370,8 @@ extern "C" int adask_pcg_restart(adask_ctx* ctx, const adask_problem* pb, const 
   ADASK_TRY(precond_apply_impl(ctx, P, r, c, d, rt, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  ADASK_CUDA(launch_pdl(k_pcg_restart_tail, dim3(1), dim3(kVecThreads), 0, st, d, c, rt, r, p, dt_col, sc));
+  ADASK_CUDA(launch_pdl(k_pcg_restart_tail, dim3(1), dim3(kVecThreads), 0, st, d, c, rt, r, p, dt_col, sc,
+                        mail_of(ctx), ctx->mail_seq));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
@@ -332,7 +394,7 @@ extern "C" int adask_pcg_propose(adask_ctx* ctx, const adask_problem* pb, const 
   k_pcg_step<<<1, kVecThreads, 0, st>>>(d, c, x, r, p, Hp, dt_col, x_new, r_new, sc);
   ADASK_LAUNCHED(ctx);
   ADASK_TRY(precond_apply_impl(ctx, P, r_new, c, d, rt_new, d, st));
-  k_pcg_scalars<<<1, kVecThreads, 0, st>>>(d, c, r_new, rt_new, dt_new, sc);
+  k_pcg_scalars<<<1, kVecThreads, 0, st>>>(d, c, r_new, rt_new, dt_new, sc, mail_of(ctx), ctx->mail_seq);
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   ADASK_TRY(read_scalars(ctx, sc, delta_tilde_host, &flags, st));
@@ -361,7 +423,8 @@ extern "C" int adask_ihs_restart(adask_ctx* ctx, const adask_problem* pb, const 
   ADASK_TRY(precond_apply_impl(ctx, P, g, c, d, v, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g, v, sc));
+  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g, v, sc, mail_of(ctx),
+                        ctx->mail_seq));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
@@ -381,7 +444,8 @@ extern "C" int adask_ihs_propose(adask_ctx* ctx, const adask_problem* pb, const 
   ADASK_TRY(precond_apply_impl(ctx, P, g_new, c, d, v_new, d, st));
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g_new, v_new, sc));
+  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, d, g_new, v_new, sc, mail_of(ctx),
+                        ctx->mail_seq));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   return read_scalars(ctx, sc, delta_tilde_host, &flags, st);
@@ -393,7 +457,8 @@ extern "C" int adask_dot(adask_ctx* ctx, const double* a, const double* b, int64
   cudaStream_t st = S(stream);
   IterScalars* sc = nullptr;
   ADASK_TRY(get_scalars(ctx, &sc, st));
-  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, ld, a, b, sc));
+  ADASK_CUDA(launch_pdl(k_half_dot, dim3(1), dim3(kVecThreads), 0, st, d, c, ld, a, b, sc, mail_of(ctx),
+                        ctx->mail_seq));
   ADASK_LAUNCHED(ctx);
   int flags = 0;
   return read_scalars(ctx, sc, result_host, &flags, st);
