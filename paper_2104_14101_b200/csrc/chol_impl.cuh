@@ -218,15 +218,15 @@ __device__ void diag_factor(double (*S)[NBP], double (*X)[NBP], const unsigned s
           }
         }
         __syncthreads();
-        const int base = jb + PW, nt = NB - base;
-        for (int e = t; e < nt * nt; e += kCholThreads) {
-          const int ii = base + e / nt, ll = base + e % nt;
-          if (ll > ii) continue;
-          double v = S[ii][ll];
+        const int base = jb + PW;
+        // 16 x 16 thread grid over the trailing triangle (no integer division)
+        for (int ii = base + (t >> 4); ii < NB; ii += 16)
+          for (int ll = base + (t & 15); ll <= ii; ll += 16) {
+            double v = S[ii][ll];
 #pragma unroll
-          for (int p = 0; p < PW; ++p) v = fma(-S[ii][jb + p], S[ll][jb + p], v);
-          S[ii][ll] = v;
-        }
+            for (int p = 0; p < PW; ++p) v = fma(-S[ii][jb + p], S[ll][jb + p], v);
+            S[ii][ll] = v;
+          }
         __syncthreads();
       }
     }
