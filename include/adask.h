@@ -204,6 +204,13 @@ int adask_hess_mult(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t
                     const double* X, int64_t c, int64_t ldx, double nu2, const double* lam,
                     const double* B, int64_t ldb, double* out, int64_t ldo, uint32_t flags,
                     void* stream);
+/* out0 = H x0, out1 = H x1 with ONE pass over A (the adaptive PCG proposal
+ * streams A once for [p, x] so that a rejected proposal's restart,
+ * solvers.py:243-248, needs no pass of its own).  Each column is bitwise
+ * adask_hess_mult's; ineligible shapes fall back to two single passes.     */
+int adask_hess_mult_pair(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                         const double* x0, const double* x1, double nu2, const double* lam, double* out0,
+                         double* out1, void* stream);
 /* out = part + nu2 lam .* X - B (B nullable), c columns of length d. */
 int adask_vec_hess_finish(adask_ctx* ctx, const double* part, int64_t d, int64_t c, int64_t ld,
                           const double* X, double nu2, const double* lam, const double* B,

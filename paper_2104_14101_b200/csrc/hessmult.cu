@@ -703,3 +703,19 @@ extern "C" int adask_vec_hess_finish(adask_ctx* ctx, const double* part, int64_t
   ADASK_TRY(use_device(ctx));
   return vec_hess_finish_impl(ctx, part, d, c, ld, X, nu2, lam, B, out, S(stream));
 }
+
+extern "C" int adask_hess_mult_pair(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                                    const double* x0, const double* x1, double nu2, const double* lam,
+                                    double* out0, double* out1, void* stream) {
+  ADASK_TRY(adask::use_device(ctx));
+  if (n < 0 || d < 1 || lda < d || !x0 || !x1 || !out0 || !out1 || !lam)
+    return adask::fail(ADASK_E_DIM, "hess_mult_pair: bad arguments");
+  if (dtype != ADASK_F64 && dtype != ADASK_F32) return adask::fail(ADASK_E_ARG, "bad dtype");
+  cudaStream_t st = adask::S(stream);
+  int fused = 0;
+  ADASK_TRY(adask::hess_mult_pair_impl(ctx, dtype, A, n, d, lda, x0, nullptr, out0, x1, nullptr, out1, nu2, lam, st,
+                                       &fused));
+  if (fused) return ADASK_OK;
+  ADASK_TRY(adask::hess_mult_impl(ctx, dtype, A, n, d, lda, x0, 1, d, nu2, lam, nullptr, d, out0, d, 0, st));
+  return adask::hess_mult_impl(ctx, dtype, A, n, d, lda, x1, 1, d, nu2, lam, nullptr, d, out1, d, 0, st);
+}
