@@ -126,6 +126,30 @@ def test_srht_pipelined_passes_bitwise(ak, n, d, m, seed, monkeypatch):
     assert np.array_equal(got, O.sketch_srht(A, m, seed))
 
 
+@pytest.mark.parametrize("pipe", ["2", "3"])
+def test_srht_pipelined_strided_rows(ak, pipe, monkeypatch):
+    """A column slice of a wider matrix (lda > d, partial last panel) through
+    the pipelined / hybrid passes: bitwise the reference on the slice."""
+    from paper_2104_14101_b200.embeddings import srht_dev
+
+    monkeypatch.setenv("ADASK_FWHT_PIPE", pipe)
+    full = np.random.default_rng(4).standard_normal((1 << 15, 64))
+    Ad = torch.from_numpy(full).cuda()[:, :37]
+    got = srht_dev(Ad, 1500, 8).cpu().numpy()
+    assert np.array_equal(got, O.sketch_srht(full[:, :37], 1500, 8))
+
+
+def test_sjlt_streamed_strided_rows(ak, monkeypatch):
+    """The streamed SJLT accumulation on a column slice (lda > d): bitwise."""
+    from paper_2104_14101_b200.embeddings import sjlt_dev
+
+    monkeypatch.setenv("ADASK_SJLT_PIPE", "2")
+    full = np.random.default_rng(6).standard_normal((40000, 96))
+    Ad = torch.from_numpy(full).cuda()[:, 16:64]
+    got = sjlt_dev(Ad, 512, 13).cpu().numpy()
+    assert np.array_equal(got, O.sketch_sjlt(full[:, 16:64], 512, 13))
+
+
 @pytest.mark.parametrize("n,d,m,seed", [(1 << 16, 40, 4096, 1), (1 << 14, 20, 1 << 14, 2), (4096, 24, 1000, 3),
                                         ((1 << 17) + 32, 16, 2000, 4), (1 << 20, 6, 600, 5)])
 def test_srht_hybrid_passes_bitwise(ak, n, d, m, seed, monkeypatch):
