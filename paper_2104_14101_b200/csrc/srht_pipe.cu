@@ -38,11 +38,6 @@ namespace {
 
 enum { P1 = 0, P2 = 1 };
 
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"((uint64_t)map), "r"(c0),
-               "r"(c1), "r"(c2)
-               : "memory");
-}
 
 // 3-D tensor-map tile load, completion on an mbarrier
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
@@ -59,7 +54,6 @@ constexpr int kSmemBudget = 220 * 1024;
 
 struct PipeArgs {
   int64_t n_items, npanels, d;
-  int pf;                   // L2 prefetch distance of the producer (items)
   int64_t n_valid;          // pass 1: rows of A (rows past it are zero padding)
   int nslots;               // pass 1: needed slots (rows of a row block that reach Z)
   // pass 1
@@ -304,13 +298,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwht_pipe(const __grid_constant
       for (int64_t i = blockIdx.x; i < n_items; i += gridDim.x, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (uint32_t)((it / STAGES) & 1);
-        // L2 prefetch a.pf items ahead (warms the TMA loads beyond the smem ring)
-        for (int f = (it == 0 ? 1 : a.pf); f <= a.pf; ++f) {
-          const int64_t ip = i + (int64_t)f * gridDim.x;
-          if (ip >= n_items) break;
-          const int64_t tp = ip / npanels;
-          tma_prefetch_3d(&smap, (int32_t)((ip - tp * npanels) * W), (int32_t)(tp * BT / E0), 0);
-        }
         if (it >= STAGES) mbar_wait(&empty[s], ph ^ 1);
         const int64_t ti = i / npanels, p = i - ti * npanels;
         const int64_t row0 = ti * BT;
@@ -723,8 +710,6 @@ int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   PipeArgs a{};
   a.d = d;
   a.nslots = (int)nslots;
-  a.pf = 0;
-  if (const char* e = getenv("ADASK_FWHT_PF")) a.pf = atoi(e);
   a.n_valid = n;
   a.sgn = sgn;
   a.lo2slot = d_plan;  // null when idx is null (identity)
