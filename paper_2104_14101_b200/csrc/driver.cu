@@ -13,10 +13,12 @@
 // allreduce hook.
 #include <chrono>
 #include <cmath>
+#include <future>
 #include <vector>
 
 #include "common.cuh"
 #include "hessmult.cuh"
+
 #include "precond.cuh"
 #include "rng.cuh"
 #include "sjlt.cuh"
@@ -67,9 +69,38 @@ struct DevBuf {
   }
 };
 
+// The SRHT's host index draw for the next potential resketch, computed on a
+// worker thread while the device runs the current iterations (its inputs --
+// the next size and seed -- are fixed in advance by the doubling rule).
+struct IdxAhead {
+  int64_t m = -1;
+  uint64_t seed = 0;
+  std::future<std::vector<int64_t>> fut;
+  void start(uint64_t s, int64_t n, int64_t mm) {
+    m = mm;
+    seed = s;
+    fut = std::async(std::launch::async, [s, n, mm]() {
+      std::vector<int64_t> idx;
+      adask_pcg64 g;
+      if (gen_from_seed(s, &g) != ADASK_OK || srht_draw_idx(&g, n, mm, &idx) != ADASK_OK) idx.clear();
+      return idx;
+    });
+  }
+  // the precomputed draw if it matches (m, seed), else empty
+  std::vector<int64_t> take(uint64_t s, int64_t mm) {
+    std::vector<int64_t> r;
+    if (fut.valid()) {
+      r = fut.get();
+      if (m != mm || seed != s) r.clear();
+    }
+    m = -1;
+    return r;
+  }
+};
+
 // SA (m x d, dtype) for the configured family at sketch seed `seed`.
 static int make_sketch(adask_ctx* ctx, const adask_problem* pb, const adask_adaptive_cfg* cfg, int64_t m,
-                       uint64_t seed, void* SA, cudaStream_t st) {
+                       uint64_t seed, void* SA, cudaStream_t st, IdxAhead* ahead = nullptr) {
   const int64_t d = pb->d;
   const size_t esz = pb->dtype == ADASK_F64 ? 8 : 4;
   switch (cfg->family) {
@@ -81,7 +112,10 @@ static int make_sketch(adask_ctx* ctx, const adask_problem* pb, const adask_adap
       if (cfg->n_total != pb->n) return fail(ADASK_E_ARG, "the global SRHT does not shard (use block SRHT)");
       adask_pcg64 g;
       ADASK_TRY(gen_from_seed(seed, &g));
-      ADASK_TRY(sketch_srht_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, &g, m, SA, d, nullptr, 0, st));
+      std::vector<int64_t> pre;
+      if (ahead) pre = ahead->take(seed, m);
+      ADASK_TRY(sketch_srht_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, &g, m, SA, d, nullptr, 0, st,
+                                 pre.empty() ? nullptr : &pre));
       break;
     }
     case ADASK_SRHT_BLOCK: {
@@ -329,6 +363,9 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
     ADASK_TRY(make_sketch_incr(ctx, pb, cfg, inc, m, nullptr, 0, sa_buf.p, st));
   else
     ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, 0), sa_buf.p, st));
+  IdxAhead ahead;
+  const bool ahead_on = cfg->family == ADASK_SRHT && !inc.on && getenv("ADASK_NO_IDX_AHEAD") == nullptr;
+  if (ahead_on) ahead.start(adask_derive_seed(cfg->seed, 1), pb->n, std::min(2 * m, cap));
   adask_precond* P = nullptr;
   int64_t info = 0;
   ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
@@ -400,7 +437,9 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
       if (inc.on)
         ADASK_TRY(make_sketch_incr(ctx, pb, cfg, inc, m, sa_buf.p, m_old, nsa.p, st));
       else
-        ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, (uint64_t)K), nsa.p, st));
+        ADASK_TRY(make_sketch(ctx, pb, cfg, m, adask_derive_seed(cfg->seed, (uint64_t)K), nsa.p, st,
+                              ahead_on ? &ahead : nullptr));
+      if (ahead_on) ahead.start(adask_derive_seed(cfg->seed, (uint64_t)K + 1), pb->n, std::min(2 * m, cap));
       std::swap(sa_buf.p, nsa.p);
       sa_slot = nslot;
       ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,

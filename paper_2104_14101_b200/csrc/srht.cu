@@ -416,9 +416,20 @@ static int fwht_select(adask_ctx* ctx, int dtype, const void* A, int64_t n, int6
   return ADASK_OK;
 }
 
+// idx = choice(n_pad, m, replace=False) after the n sign draws of generator g
+// (host integer bookkeeping; the native driver precomputes it for the next
+// potential resketch on a worker thread)
+int srht_draw_idx(const adask_pcg64* g, int64_t n, int64_t m, std::vector<int64_t>* idx) {
+  const int64_t n_pad = 1ll << ilog2(n);
+  adask_pcg64 h = *g;
+  adask_pcg64_skip_u32(&h, (uint64_t)n);
+  idx->assign((size_t)m, 0);
+  return adask_choice_noreplace(&h, n_pad, m, idx->data());
+}
+
 int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                      const adask_pcg64* g, int64_t m, void* SA, int64_t ldsa, int64_t* idx_host,
-                     uint32_t flags, cudaStream_t st) {
+                     uint32_t flags, cudaStream_t st, const std::vector<int64_t>* idx_pre) {
   if (m < 1) return fail(ADASK_E_SKETCH_TOO_LARGE, "sketch size must be a positive integer, got %lld",
                          (long long)m);
   if (n < 1 || d < 1 || lda < d || ldsa < d) return fail(ADASK_E_DIM, "sketch_srht: bad shape");
@@ -435,10 +446,9 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   uint32_t* sgn = (uint32_t*)sw;
   ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
   // idx = choice(n_pad, m, replace=False) after the n sign draws (host)
-  adask_pcg64 h = *g;
-  adask_pcg64_skip_u32(&h, (uint64_t)n);
-  std::vector<int64_t> idx((size_t)m);
-  ADASK_TRY(adask_choice_noreplace(&h, n_pad, m, idx.data()));
+  std::vector<int64_t> idx_own;
+  if (!idx_pre || (int64_t)idx_pre->size() != m) ADASK_TRY(srht_draw_idx(g, n, m, &idx_own));
+  const std::vector<int64_t>& idx = (idx_pre && (int64_t)idx_pre->size() == m) ? *idx_pre : idx_own;
   if (idx_host) std::copy(idx.begin(), idx.end(), idx_host);
   const double c1 = sqrt((double)n_pad);
   const double c2 = sqrt((double)n_pad / (double)m);

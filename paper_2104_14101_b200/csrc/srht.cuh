@@ -1,10 +1,14 @@
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 
 namespace adask {
 int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                      const adask_pcg64* g, int64_t m, void* SA, int64_t ldsa, int64_t* idx_host,
-                     uint32_t flags, cudaStream_t st);
+                     uint32_t flags, cudaStream_t st, const std::vector<int64_t>* idx_pre = nullptr);
+// choice(n_pad, m) after the n sign draws of g (the SRHT's host index draw)
+int srht_draw_idx(const adask_pcg64* g, int64_t n, int64_t m, std::vector<int64_t>* idx);
 // Incremental growth: the full normalized transform Y (n_pad x d, ld d) at
 // the generator's signs, and the draw order perm (n_pad entries, host);
 // then SA (+)= Y[perm[:m]] sqrt(n_pad / m).
