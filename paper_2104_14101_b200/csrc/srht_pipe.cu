@@ -6,20 +6,22 @@
 //
 //   * persistent CTAs (one per SM), items = (row tile, column panel), column
 //     panels fastest so the grid sweeps whole rows of A together;
-//   * a producer warp streams each tile (BT rows x one 32/64-byte column
-//     segment) into a STAGES-deep shared-memory ring with TMA 2-D tensor loads
-//     (rows past n arrive as zeros = the reference's zero padding) and, in
-//     pass 2, the tile's slice of the output-row map with a bulk copy;
-//   * 8 consumer warps run the butterflies in place in the stage: 5-bit
-//     register rounds, one named barrier between rounds, and emit straight to
-//     global memory from registers (pass 1: the needed slots of Z; pass 2: the
-//     selected rows of SA, scaled exactly as the reference's two steps);
-//   * shared-memory banks: a tile row is 32 or 64 bytes, so the units a warp
-//     reads together must sit on different bank groups.  In rounds >= 1 the
-//     warp's units differ in the low row bits already; in round 0 (rows
-//     q*E + e) unit q walks its rows in the order e ^ X, X = q mod (128/SEGB),
-//     and the first log2(128/SEGB) butterfly stages swap their operands where
-//     X says so -- the same additions and subtractions, bit for bit.
+//   * a producer warp streams each 1024-row x 64-byte tile into a 2-stage
+//     shared-memory ring with ONE 3-D TMA tensor-map load (the view
+//     {columns, row/32, row%32} lands the tile as [e][q], row q*32 + e; rows
+//     past n arrive as zeros = the reference's zero padding) plus, by bulk
+//     copy, the tile's sign words (pass 1) or its slice of the output-row map
+//     (pass 2);
+//   * 8 consumer warps run bits 0-4 in registers straight from the stage
+//     (fp32 as packed pairs: one FADD2 per two butterflies), release it, and
+//     run bits 5-9 in a scratch tile whose rows are permuted r ^ ((r>>5)&3) so
+//     that every warp access covers the four 32-byte bank groups;
+//   * emit: pass 1 writes Z straight from registers when every slot is
+//     needed, else copies out only the needed slots; pass 2 copies out the
+//     selected rows, scaled exactly as the reference's two steps (or writes the
+//     two half transforms of an 11-bit pass 2, combined by k_srht_combine);
+//   * fp64 with m >= 512 hands Z to the tile kernel's pass 2 (srht.cu), which
+//     is faster on the short 2^(L-10)-point transforms.
 //
 // Bytes: pass 1 reads n_pad x d (A, zero rows free) and writes nslots*G x d of
 // Z; pass 2 reads Z and writes m x d.  Both passes are HBM streams.
