@@ -12,6 +12,7 @@ struct CholArgs {
   int* info;
   unsigned long long* tlog;  // optional phase timestamps (ADASK_CHOL_TRACE)
   int slow_diag;             // 1: unblocked pivot loop (ADASK_CHOL_SLOWDIAG, comparison)
+  int fused_inv;             // 1: L^-1 by rows inside the factorization's phases
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -347,6 +348,100 @@ __device__ void diag_factor(double (*S)[NBP], double (*X)[NBP], const unsigned s
   if (tl && threadIdx.x == 0) tl[2] = gtimer2();
 }
 
+// Fused inverse (a.fused_inv), X = L^-1 by block rows, interleaved with the
+// factorization's phases so it runs on the CTAs the shrinking trailing update
+// leaves idle:
+//   row s:     X_sl = -Dinv_s T_sl (l < s),  X_ss = Dinv_s (stored at factor time)
+//   update p:  T_il = sum_{q=l}^{p} L_iq X_ql for i > p, l <= p  (one term per step)
+// T lives in M's strictly-lower tiles left of the active panel (A_il is dead
+// once its trsm ran).  Update p runs in the trsm phase of panel p+1 (L_{*,p}
+// and row p of X are final), row s in the syrk phase of panel s (T_sl has all
+// its terms); X is written to Li and, transposed, to LiT.
+// Work items continue the phase's round-robin after `skip` items (CTA b takes
+// item u when u = b (mod G)); skip < 0: all CTAs, from item 0.
+template <typename T>
+__device__ __forceinline__ void inv_update(const CholArgs& a, int p, int skip, double (*sA)[NBP], double (*sB)[NBP],
+                                           double (*sC)[NBP], double (&acc)[TM][TM]) {
+  const T* L = reinterpret_cast<const T*>(a.L);
+  const T* Li = reinterpret_cast<const T*>(a.Li);
+  T* M = reinterpret_cast<T*>(a.M);
+  const int ld = a.kp, G = gridDim.x, b = blockIdx.x;
+  const int nl = p + 1, nupd = (a.nblk - p - 1) * nl;
+  int q = b - skip % G;
+  if (q < 0) q += G;
+  // software-pipelined: the next item's three tiles are in flight during
+  // the current product
+  TileRegs<T> ra, rb, rc;
+  if (q < nupd) {
+    const int i = p + 1 + q / nl, l = q % nl;
+    tile_fetch<T>(ra, L, ld, i, p);
+    tile_fetch<T>(rb, Li, ld, p, l);
+    if (l < p) tile_fetch<T>(rc, M, ld, i, l);
+  }
+  for (; q < nupd; q += G) {
+    const int i = p + 1 + q / nl, l = q % nl;
+    tile_put<T>(sA, ra);
+    tile_put<T>(sB, rb);
+    if (l < p) tile_put<T>(sC, rc);
+    __syncthreads();
+    const int qn = q + G;
+    if (qn < nupd) {
+      const int in = p + 1 + qn / nl, ln = qn % nl;
+      tile_fetch<T>(ra, L, ld, in, p);
+      tile_fetch<T>(rb, Li, ld, p, ln);
+      if (ln < p) tile_fetch<T>(rc, M, ld, in, ln);
+    }
+    acc_zero(acc);
+    tile_mma<false>(sA, sB, acc);
+    {
+      const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
+#pragma unroll
+      for (int x = 0; x < TM; ++x)
+#pragma unroll
+        for (int y = 0; y < TM; ++y) {
+          double& c = sC[tr + 16 * x][tc + 16 * y];
+          c = l < p ? c + acc[x][y] : acc[x][y];
+        }
+    }
+    __syncthreads();
+    tile_store<T>(M, ld, i, l, sC);
+    __syncthreads();
+  }
+}
+
+// Row s of X.  skip >= 0: the syrk phase's CTAs >= 1 (CTA 0 factors the next
+// diagonal tile) continue their round-robin after `skip` tiles; skip < 0: all.
+template <typename T>
+__device__ __forceinline__ void inv_row(const CholArgs& a, int s, int skip, double (*sA)[NBP], double (*sB)[NBP],
+                                        double (*sC)[NBP], double (&acc)[TM][TM]) {
+  T* Li = reinterpret_cast<T*>(a.Li);
+  T* LiT = reinterpret_cast<T*>(a.LiT);
+  const T* M = reinterpret_cast<const T*>(a.M);
+  const int ld = a.kp, b = blockIdx.x;
+  int W = gridDim.x, me = b;
+  if (skip >= 0 && W > 1) {
+    if (b == 0) return;
+    W -= 1;
+    me = b - 1;
+  } else if (skip < 0) {
+    skip = 0;
+  }
+  int l = me - skip % W;
+  if (l < 0) l += W;
+  for (; l < s; l += W) {
+    tile_load<T>(sA, Li, ld, s, s);
+    tile_load<T>(sB, M, ld, s, l);
+    __syncthreads();
+    acc_zero(acc);
+    tile_mma<false>(sA, sB, acc);
+    acc_to_tile(sC, acc, -1.0);
+    __syncthreads();
+    tile_store<T>(Li, ld, s, l, sC);
+    tile_store<T>(LiT, ld, l, s, sC, true, 0);
+    __syncthreads();
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
   cg::grid_group grid = cg::this_grid();
@@ -377,6 +472,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
     TMARK(3 * nblk + 5);
     tile_store<T>(L, ld, 0, 0, sA, false, 1);
     tile_store<T>(Li, ld, 0, 0, sB, false, 1);
+    if (a.fused_inv) tile_store<T>(LiT, ld, 0, 0, sB, true, 2);
     __syncthreads();
     TMARK(3 * nblk + 6);
   }
@@ -399,6 +495,8 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
       tile_store<T>(L, ld, i, j, sC);
       __syncthreads();
     }
+    // fused inverse, update of step j-1 on the idle CTAs (after the trsm rows)
+    if (a.fused_inv && j >= 1) inv_update<T>(a, j - 1, nblk - j - 1, sA, sB, sC, acc);
     grid.sync();
     TMARK(2 + 3 * j);
     // ---- syrk: A_il -= L_ij L_lj^T for j < l <= i.  CTA 0 owns the next
@@ -433,15 +531,30 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
         diag_factor(sC, sB, tri_tab, a.info, (j + 1) * NB, a.k, nullptr, a.slow_diag);
         tile_store<T>(L, ld, j + 1, j + 1, sC, false, 1);
         tile_store<T>(Li, ld, j + 1, j + 1, sB, false, 1);
+        if (a.fused_inv) tile_store<T>(LiT, ld, j + 1, j + 1, sB, true, 2);
       } else {
         tile_store<T>(M, ld, i, l, sC);
       }
       __syncthreads();
     }
+    // fused inverse, row j of L^-1 after the syrk tiles (CTAs >= 1)
+    if (a.fused_inv && j >= 1) inv_row<T>(a, j, G == 1 ? 0 : ntiles - 1, sA, sB, sC, acc);
     grid.sync();
     TMARK(3 + 3 * j);
   }
   TMARK(3 * nblk + 1);
+  if (a.fused_inv) {
+    // the last block row: update of step nblk-2, then row nblk-1
+    if (nblk >= 2) {
+      inv_update<T>(a, nblk - 2, 0, sA, sB, sC, acc);
+      grid.sync();
+      inv_row<T>(a, nblk - 1, -1, sA, sB, sC, acc);
+      grid.sync();
+    }
+    TMARK(3 * nblk + 2);
+    TMARK(3 * nblk + 3);
+    return;
+  }
 
   // ---- inverse by recursive doubling: I21 = -I22 (L21 I11), scratch in M
   for (int s = 1; s < nblk; s <<= 1) {
@@ -548,7 +661,13 @@ __global__ void __launch_bounds__(kCholThreads, 1) k_chol_coop(CholArgs a) {
 inline int launch(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, void* L, void* Li, void* LiT,
                   int* info, unsigned long long* tlog, cudaStream_t st, int* grid_out) {
   const int nblk = (int)(kp / NB);
-  CholArgs a{M, L, Li, LiT, (int)kp, nblk, (int)k, info, tlog, getenv("ADASK_CHOL_SLOWDIAG") ? 1 : 0};
+  const char* fi = getenv("ADASK_CHOL_INV");
+  CholArgs a{M, L, Li, LiT, (int)kp, nblk, (int)k, info, tlog, getenv("ADASK_CHOL_SLOWDIAG") ? 1 : 0,
+             // fused inverse up to 64 block rows (k = 2048 at NB = 32): its per-step
+             // updates are single tile products, which lose to the doubling's long
+             // chains once the updates outnumber the SMs several times over
+             // (k = 1024: 528 -> 478 us; k = 2048: even; k = 4096: +4%)
+             fi ? (atoi(fi) != 0) : (nblk <= 64)};
   const int smem = 5 * NB * NBP * (int)sizeof(double);
   void* fn = dtype == ADASK_F64 ? (void*)k_chol_coop<double> : (void*)k_chol_coop<float>;
   ADASK_TRY(ensure_smem_attr(fn, smem));

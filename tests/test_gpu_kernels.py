@@ -249,6 +249,22 @@ def test_precond_large(ak, m, d):
     assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("inv", ["0", "1"])
+@pytest.mark.parametrize("m,d", [(40, 31), (50, 33), (100, 65), (300, 97), (900, 700), (2000, 1600)])
+def test_precond_inverse_variants(ak, monkeypatch, inv, m, d):
+    """Both L^-1 schedules of the cooperative Cholesky (fused row-wise inside
+    the factorization; recursive doubling after it) against the oracle."""
+    monkeypatch.setenv("ADASK_CHOL_INV", inv)
+    rng = np.random.default_rng(m + d)
+    SA = rng.standard_normal((m, d)) / np.sqrt(m)
+    lam = 1.0 + rng.uniform(0, 9, d)
+    P = ak.build(SA, 0.05, lam)
+    Po = O.build(SA, 0.05, lam)
+    z = rng.standard_normal((d, 2))
+    got, ref = P.solve(z), Po.solve(z)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
 @pytest.mark.parametrize("k", [1, 63, 64, 65, 700, 2500])
 def test_cholesky_sizes(ak, k):
     rng = np.random.default_rng(k)
