@@ -142,6 +142,10 @@ struct adask_ctx {
   // the host spins on the sequence number (no copy-engine D2H, no stream sync)
   void* mail = nullptr;
   uint32_t mail_seq = 0;
+  // profiled pass only: pinned gate word [0] = released sequence, [1] = timeouts
+  // (adask::prof_gate_hold; ADASK_PROF_GATE=0 turns the gate off)
+  uint32_t* gate = nullptr;
+  uint32_t gate_seq = 0;
 };
 
 namespace adask {
@@ -181,25 +185,35 @@ int upload_async(adask_ctx* ctx, void* dst, const void* src, size_t bytes, cudaS
 // path the GPU idles while the host issues the next kernel.
 int ensure_smem_attr(const void* fn, int bytes);
 // RAII timing scope for one unit; no-op unless profiling is enabled.
+// Gate for a unit whose host side plans between its launches: a one-warp
+// kernel holds the stream until the unit is fully enqueued (host release, or
+// a 20 ms timeout), so the unit's event window holds its device work only,
+// not host enqueue gaps after a decision sync left the stream empty.
+int prof_gate_hold(adask_ctx* ctx, cudaStream_t st);
+bool prof_gate_enabled();
+
 struct ProfScope {
   adask_ctx* ctx;
   int kind;
   cudaStream_t st;
   adask_prof_rec rec{};
   bool on;
-  ProfScope(adask_ctx* c, int k, cudaStream_t s, double bytes, double flops = 0.0)
+  bool gated = false;
+  ProfScope(adask_ctx* c, int k, cudaStream_t s, double bytes, double flops = 0.0, bool gate = false)
       : ctx(c), kind(k), st(s), on(c && c->prof) {
     if (!on) return;
     rec.a = take();
     rec.b = take();
     rec.bytes = bytes;
     rec.flops = flops;
+    if (gate && prof_gate_enabled()) gated = prof_gate_hold(ctx, st) == 0;
     cudaEventRecord(rec.a, st);
   }
   ~ProfScope() {
     if (!on) return;
     cudaEventRecord(rec.b, st);
     ctx->prof_recs[kind].push_back(rec);
+    if (gated) __atomic_store_n(&ctx->gate[0], ctx->gate_seq, __ATOMIC_RELEASE);
   }
   cudaEvent_t take() {
     cudaEvent_t e;

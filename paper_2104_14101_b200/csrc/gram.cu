@@ -4,6 +4,7 @@
 // for the hand-written register-blocked kernel (gemm.cu) they replace here.
 // Row-major buffers are read as their column-major transposes; no TF32.
 #include <cublas_v2.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -59,7 +60,29 @@ int gram_dense(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t d, 
   // column-major X = SA^T (d x m, ld = ldsa); C = X X^T, column-major upper =
   // row-major lower.  Up to d = 1024 cuBLAS' GEMM (full square) is faster
   // than its SYRK on this GPU (measured: tools/gemm_probe.py), above it SYRK.
-  if (d <= 1024) {
+  const bool split = !(getenv("ADASK_GRAM_SPLIT") && atoi(getenv("ADASK_GRAM_SPLIT")) == 0);
+  if (d <= 1024 && split && d >= 256 && m >= 2048) {
+    // only the lower triangle (row-major) is consumed: C[:, d1:] = X X2^T and
+    // C11 = X1 X1^T, 3/4 of the square's flops in two GEMMs (measured at
+    // d = 1024: m = 2048 / 4096 fp64 builds 0.69 -> 0.67 / 0.80 -> 0.75 ms,
+    // m = 32768 fp32 1.76 -> 1.59 ms; no gain below m = 2048)
+    const int d1 = (int)(d / 2 / 16 * 16), d2 = (int)d - d1;
+    if (dtype == ADASK_F64) {
+      const double one = 1.0, zero = 0.0;
+      const double* X = (const double*)SA;
+      ADASK_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)d, d2, (int)m, &one, X, (int)ldsa, X + d1, (int)ldsa,
+                             &zero, (double*)M + (int64_t)d1 * ldm, (int)ldm));
+      ADASK_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, d1, d1, (int)m, &one, X, (int)ldsa, X, (int)ldsa, &zero,
+                             (double*)M, (int)ldm));
+    } else {
+      const float one = 1.0f, zero = 0.0f;
+      const float* X = (const float*)SA;
+      ADASK_BLAS(cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)d, d2, (int)m, &one, X, (int)ldsa, X + d1, (int)ldsa,
+                             &zero, (float*)M + (int64_t)d1 * ldm, (int)ldm));
+      ADASK_BLAS(cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, d1, d1, (int)m, &one, X, (int)ldsa, X, (int)ldsa, &zero,
+                             (float*)M, (int)ldm));
+    }
+  } else if (d <= 1024) {
     if (dtype == ADASK_F64) {
       const double one = 1.0, zero = 0.0;
       ADASK_BLAS(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)d, (int)d, (int)m, &one, (const double*)SA,

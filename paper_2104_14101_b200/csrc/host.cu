@@ -378,6 +378,7 @@ int adask_ctx_destroy(adask_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
   if (ctx->mail) cudaFreeHost(ctx->mail);
+  if (ctx->gate) cudaFreeHost(ctx->gate);
   for (auto& b : ctx->stage) {
     if (b.ev) {
       cudaEventSynchronize(b.ev);
@@ -415,6 +416,45 @@ int upload_async(adask_ctx* ctx, void* dst, const void* src, size_t bytes, cudaS
   ADASK_CUDA(cudaMemcpyAsync(dst, b.p, bytes, cudaMemcpyHostToDevice, st));
   ADASK_CUDA(cudaEventRecord(b.ev, st));
   b.pending = true;
+  return ADASK_OK;
+}
+
+__global__ void k_prof_gate(volatile uint32_t* g, uint32_t seq, unsigned long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  while ((int32_t)(g[0] - seq) < 0) {
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      g[1] = g[1] + 1;
+      break;
+    }
+    __nanosleep(256);
+  }
+}
+
+bool prof_gate_enabled() {
+  static const bool on = !(getenv("ADASK_PROF_GATE") && atoi(getenv("ADASK_PROF_GATE")) == 0);
+  return on;
+}
+
+int prof_gate_hold(adask_ctx* ctx, cudaStream_t st) {
+  if (!ctx->gate) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, 64) != cudaSuccess) {
+      cudaGetLastError();
+      return ADASK_E_CUDA;
+    }
+    memset(p, 0, 64);
+    ctx->gate = (uint32_t*)p;
+    ctx->gate_seq = 0;
+  }
+  ++ctx->gate_seq;
+  k_prof_gate<<<1, 32, 0, st>>>(ctx->gate, ctx->gate_seq, 20000000ull);
+  if (cudaGetLastError() != cudaSuccess) {
+    __atomic_store_n(&ctx->gate[0], ctx->gate_seq, __ATOMIC_RELEASE);
+    return ADASK_E_CUDA;
+  }
   return ADASK_OK;
 }
 

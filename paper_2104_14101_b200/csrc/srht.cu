@@ -18,6 +18,7 @@
 // Algorithmic bytes: (n + m) * d * sizeof(T); the pruned intermediate adds
 // 2 * nslots * G * d * sizeof(T) (nslots <= min(m, B)).
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <vector>
 
@@ -439,7 +440,9 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
     return fail(ADASK_E_SKETCH_TOO_LARGE, "m = %lld exceeds padded row count %lld", (long long)m,
                 (long long)n_pad);
   if (ilog2(n_pad) > 24) return fail(ADASK_E_ARG, "sketch_srht: n_pad > 2^24 unsupported");
-  ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4));
+  static const bool htrace = getenv("ADASK_HOST_TRACE") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4), 0.0, true);
   // signs: draws [0, n) of integers(0, 2)
   void* sw = nullptr;
   ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(1ll << ilog2(n), 32) * 4 + 64, st, &sw));  // padded: bulk-copied per tile
@@ -452,8 +455,17 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   if (idx_host) std::copy(idx.begin(), idx.end(), idx_host);
   const double c1 = sqrt((double)n_pad);
   const double c2 = sqrt((double)n_pad / (double)m);
-  return fwht_select(ctx, dtype, A, n, d, lda, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2,
-                     (flags & ADASK_ACCUMULATE) ? 1 : 0, st);
+  const auto h1 = std::chrono::steady_clock::now();
+  const int rc = fwht_select(ctx, dtype, A, n, d, lda, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2,
+                             (flags & ADASK_ACCUMULATE) ? 1 : 0, st);
+  if (htrace) {
+    const auto h2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[srht host] m=%lld pre=%d signs+draw %.1f us, fwht_select %.1f us\n", (long long)m,
+            idx_pre && (int64_t)idx_pre->size() == m ? 1 : 0,
+            std::chrono::duration<double, std::micro>(h1 - h0).count(),
+            std::chrono::duration<double, std::micro>(h2 - h1).count());
+  }
+  return rc;
 }
 
 // ---------------------------------------------------- incremental sketch growth

@@ -49,12 +49,13 @@ def traffic(rep, pat):
 P = "gpurun_out/prof/"
 t1 = traffic(P + "cfg1_full.ncu-rep", "k_hess_tma")
 t4 = traffic(P + "cfg4_srht_m4096.ncu-rep", "k_")
-out = {"cfg1": {"hess_mult": sum(t1) / len(t1), "srht": None},
+t1s = traffic(P + "cfg1_full.ncu-rep", "k_fwht")  # pass 1, pass 2 of the first sketch, ...
+out = {"cfg1": {"hess_mult": sum(t1) / len(t1), "srht": t1s[0] + t1s[1] if len(t1s) >= 2 else None},
        "cfg2": {"sjlt": sum(traffic(P + "cfg2_sjlt_full.ncu-rep", "k_sjlt_pipe"))},
        "cfg3": {"gaussian": sum(traffic(P + "cfg3_tc_full.ncu-rep", "k_gauss_tc"))},
        "cfg4": {"srht": sum(t4)},
        "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes) of the roofline unit, from "
-               "profiles/r01_ncu_full_summary.md (cfg1: hess_mult mean; cfg2: SJLT accumulation m=2048; cfg3: TF32 "
+               "profiles/r01_ncu_full_summary.md (cfg1: hess_mult mean, srht = both passes of the first sketch (m = 32); cfg2: SJLT accumulation m=2048; cfg3: TF32 "
                "sketch m=2048; cfg4: both SRHT passes + combine of one 2^21-row block at m=4096)"}
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
 print(out)
