@@ -242,6 +242,15 @@ int adask_precond_copy_factor(adask_ctx* ctx, const adask_precond* P, int which,
  * Preconditioner.sketched_hessian (preconditioner.py:55-57).               */
 int adask_gram(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                double nu2, const double* lam, void* out, int64_t ldo, void* stream);
+/* The same with an explicit output dtype: fp32 A with an fp64 result
+ * (accumulated in fp64) is the exact Hessian of direct_solve for fp32 data
+ * (problem.py:144-149 with the reference's float64 cast, problem.py:51).    */
+int adask_gram_ex(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                  double nu2, const double* lam, int out_dtype, void* out, int64_t ldo, void* stream);
+/* Woodbury capacitance W_S = (SA * (1/lam)) SA^T + nu2 I (m x m, symmetric,
+ * dtype), the matrix build() factors when m < d (preconditioner.py:72-73). */
+int adask_gram_woodbury(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t d, int64_t ldsa,
+                        double nu2, const double* lam, void* out, int64_t ldo, void* stream);
 /* out = H_S^{-1} Z (preconditioner.py:42-53), c columns. */
 int adask_precond_apply(adask_ctx* ctx, const adask_precond* P, const double* Z, int64_t c,
                         int64_t ldz, double* out, int64_t ldo, void* stream);

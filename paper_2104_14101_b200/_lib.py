@@ -140,6 +140,8 @@ _PROTOS = {
     "adask_precond_apply": (C.c_int, [vp, vp, vp, i64, i64, vp, i64, vp]),
     "adask_precond_copy_factor": (C.c_int, [vp, vp, C.c_int, vp, i64, vp]),
     "adask_gram": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, dbl, vp, vp, i64, vp]),
+    "adask_gram_ex": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, dbl, vp, C.c_int, vp, i64, vp]),
+    "adask_gram_woodbury": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, dbl, vp, vp, i64, vp]),
     "adask_cholesky": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, P(i64), vp]),
     "adask_tri_solve": (C.c_int, [vp, C.c_int, vp, i64, i64, C.c_int, vp, i64, i64, vp, i64, vp]),
     "adask_pcg_restart": (C.c_int, [vp, P(Problem), vp, vp, vp, vp, vp, vp, P(dbl), vp]),

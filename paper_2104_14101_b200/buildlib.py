@@ -77,9 +77,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if LIB.exists() and not force and all(o.stat().st_mtime <= LIB.stat().st_mtime for o in objs):
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    # cuBLAS (plain library SYRK / GEMM for the preconditioner Grams) is linked
-    # dynamically; its soname is shared with the copy torch loads
-    cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static", "-lcublas", "-lrt",
+    cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart_static", "-lrt",
            "-ldl", "-lpthread", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

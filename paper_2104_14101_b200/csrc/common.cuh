@@ -93,6 +93,8 @@ enum WsSlot {
   WS_SA0,        // native driver: the current sketch SA (referenced by the live preconditioner)
   WS_SA1,        // native driver: the next sketch
   WS_SRHT_U,     // pipelined SRHT: the two half transforms of an 11-bit pass 2
+  WS_GRAM_PACK,  // Gram: 16-byte aligned copy of an odd-shaped operand
+  WS_GRAM_RL,    // Gram: 1/lam (Woodbury scaling), zero padded
   WS_COUNT
 };
 
@@ -125,7 +127,6 @@ struct adask_ctx {
   int prof = 0;
   std::vector<adask_prof_rec> prof_recs[adask::PK_COUNT];
   std::vector<cudaEvent_t> event_pool;
-  void* blas = nullptr;  // cublasHandle_t, created on first Gram (gram.cu)
   // native driver: the Cholesky's pivot check is read at the driver's next
   // stream synchronization instead of a sync of its own (pinned_flags[1])
   bool defer_spd = false;

@@ -374,7 +374,6 @@ int adask_ctx_destroy(adask_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (auto& w : ctx->ws) w.release();
-  adask::blas_release(ctx);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
   if (ctx->mail) cudaFreeHost(ctx->mail);

@@ -16,11 +16,6 @@
 
 namespace adask {
 
-__global__ void k_recip(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = 1.0 / v[i];
-}
-
 int precond_apply_impl(adask_ctx* ctx, const adask_precond* P, const double* Z, int64_t c,
                        int64_t ldz, double* out, int64_t ldo, cudaStream_t st) {
   if (!P) return fail(ADASK_E_ARG, "null preconditioner");
@@ -111,26 +106,12 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
     s = ctx->ws[WS_GRAM].get(gram_bytes + (size_t)d * sizeof(double), st, &wsp);
     if (s) break;
     void* M = wsp;
-    double* kinv = (double*)((char*)wsp + gram_bytes);
-    const bool native = getenv("ADASK_GRAM_NATIVE") != nullptr;  // hand-written GEMM (comparison)
     if (P->path == 0) {
       // H_S = SA^T SA + nu^2 diag(lam)   (preconditioner.py:70)
-      s = native ? gemm_impl(ctx, dtype, d, d, m, 1.0, SA, ldsa, true, SA, ldsa, false, nullptr, 0.0, M, kp,
-                             P->nu2, P->lam, true, st)
-                 : gram_dense(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
-    } else if (!native) {
-      // W_S = (SA / lam) SA^T + nu^2 I   (preconditioner.py:72-73)
-      s = gram_woodbury(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
+      s = gram_dense(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
     } else {
-      k_recip<<<(unsigned)cdiv(d, 256), 256, 0, st>>>(P->lam, d, kinv);
-      cudaError_t le = cudaGetLastError();
-      if (le != cudaSuccess) {
-        s = fail(ADASK_E_CUDA, "k_recip: %s", cudaGetErrorString(le));
-        break;
-      }
-      ctx->launches++;
-      s = gemm_impl(ctx, dtype, m, m, d, 1.0, SA, ldsa, false, SA, ldsa, true, kinv, 0.0, M, kp,
-                    P->nu2, nullptr, true, st);
+      // W_S = (SA * (1/lam)) SA^T + nu^2 I   (preconditioner.py:72-73)
+      s = gram_woodbury(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
     }
     if (s) break;
     s = pad_identity(ctx, dtype, M, k, kp, st);
@@ -185,14 +166,38 @@ __global__ void k_mirror_lower(T* M, int64_t k, int64_t ld) {
 
 extern "C" int adask_gram(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                           double nu2, const double* lam, void* out, int64_t ldo, void* stream) {
+  return adask_gram_ex(ctx, dtype, A, n, d, lda, nu2, lam, dtype, out, ldo, stream);
+}
+
+extern "C" int adask_gram_ex(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                             double nu2, const double* lam, int out_dtype, void* out, int64_t ldo, void* stream) {
   ADASK_TRY(use_device(ctx));
   if (n < 0 || d < 1 || lda < d || ldo < d) return fail(ADASK_E_DIM, "gram: bad shape");
+  if ((dtype != ADASK_F64 && dtype != ADASK_F32) || (out_dtype != ADASK_F64 && out_dtype != ADASK_F32) ||
+      (dtype == ADASK_F64 && out_dtype == ADASK_F32))
+    return fail(ADASK_E_ARG, "gram: unsupported dtype pair");
   cudaStream_t st = S(stream);
-  ADASK_TRY(gram_dense(ctx, dtype, A, n, d, lda, lam ? nu2 : 0.0, lam, out, ldo, st));
-  if (dtype == ADASK_F64)
+  ADASK_TRY(gram::gram_tc(ctx, dtype, A, lda, n, d, false, nullptr, lam ? nu2 : 0.0, lam, out, ldo,
+                          out_dtype == ADASK_F64 && dtype == ADASK_F32, st));
+  if (out_dtype == ADASK_F64)
     k_mirror_lower<double><<<(unsigned)cdiv(d * d, 256), 256, 0, st>>>((double*)out, d, ldo);
   else
     k_mirror_lower<float><<<(unsigned)cdiv(d * d, 256), 256, 0, st>>>((float*)out, d, ldo);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
+extern "C" int adask_gram_woodbury(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t d, int64_t ldsa,
+                                   double nu2, const double* lam, void* out, int64_t ldo, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (m < 1 || d < 1 || ldsa < d || ldo < m || !lam) return fail(ADASK_E_DIM, "gram_woodbury: bad shape");
+  if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
+  cudaStream_t st = S(stream);
+  ADASK_TRY(gram_woodbury(ctx, dtype, SA, m, d, ldsa, nu2, lam, out, ldo, st));
+  if (dtype == ADASK_F64)
+    k_mirror_lower<double><<<(unsigned)cdiv(m * m, 256), 256, 0, st>>>((double*)out, m, ldo);
+  else
+    k_mirror_lower<float><<<(unsigned)cdiv(m * m, 256), 256, 0, st>>>((float*)out, m, ldo);
   ADASK_LAUNCHED(ctx);
   return ADASK_OK;
 }

@@ -107,7 +107,7 @@ class Preconditioner:
 
 
 def gram_dev(A: torch.Tensor, nu2: float, lam: torch.Tensor | None) -> torch.Tensor:
-    """Dense symmetric A.T A + nu2 diag(lam) on the device (libadask GEMM)."""
+    """Dense symmetric A.T A + nu2 diag(lam) on the device (libadask DMMA Gram)."""
     A = A.contiguous()
     n, d = A.shape
     H = torch.empty((d, d), dtype=A.dtype, device=A.device)
@@ -115,6 +115,17 @@ def gram_dev(A: torch.Tensor, nu2: float, lam: torch.Tensor | None) -> torch.Ten
                                      A.stride(0), float(nu2), None if lam is None else lam.data_ptr(),
                                      H.data_ptr(), d, dv.stream()), "gram")
     return H
+
+
+def woodbury_gram_dev(SA: torch.Tensor, nu2: float, lam: torch.Tensor) -> torch.Tensor:
+    """W_S = (SA * (1/lam)) SA^T + nu2 I (preconditioner.py:72-73), symmetric m x m."""
+    SA = SA if SA.stride(1) == 1 else SA.contiguous()
+    m, d = SA.shape
+    W = torch.empty((m, m), dtype=SA.dtype, device=SA.device)
+    _lib.check(_lib.lib().adask_gram_woodbury(dv.ctx().handle, dv.dtype_code(SA.dtype), SA.data_ptr(), m, d,
+                                              SA.stride(0), float(nu2), lam.data_ptr(), W.data_ptr(), m,
+                                              dv.stream()), "gram_woodbury")
+    return W
 
 
 def build_dev(SA_dev: torch.Tensor, nu: float, lam_dev: torch.Tensor, like=None) -> Preconditioner:

@@ -181,20 +181,15 @@ def direct_solve(p: RegularizedProblem) -> ExactSolution:
     return ExactSolution(x_star=dv.to_host_like(X, p._like))
 
 
-def gram_fp64(A: torch.Tensor, nu2: float = 0.0, lam: torch.Tensor | None = None,
-              rows: int = 1 << 16) -> torch.Tensor:
-    """A^T A (+ nu2 diag(lam)) in fp64 for an fp32 or fp64 A, over row blocks."""
+def gram_fp64(A: torch.Tensor, nu2: float = 0.0, lam: torch.Tensor | None = None) -> torch.Tensor:
+    """A^T A (+ nu2 diag(lam)) in fp64 for an fp32 or fp64 A: one DMMA Gram
+    (fp32 entries widened at the fragment load, fp64 accumulation)."""
+    A = A if A.stride(1) == 1 else A.contiguous()
     n, d = A.shape
-    H = torch.zeros((d, d), dtype=dv.F64, device=A.device)
-    part = torch.empty_like(H)
-    for r0 in range(0, n, rows):
-        blk = A[r0:r0 + rows]
-        blk = blk if blk.dtype == dv.F64 else blk.double()
-        _lib.check(_lib.lib().adask_gram(dv.ctx().handle, dv.dtype_code(dv.F64), blk.data_ptr(), blk.shape[0], d,
-                                         blk.stride(0), 0.0, None, part.data_ptr(), d, dv.stream()), "gram")
-        H += part
-    if lam is not None and nu2 != 0.0:
-        H.diagonal().add_(nu2 * lam)
+    H = torch.empty((d, d), dtype=dv.F64, device=A.device)
+    _lib.check(_lib.lib().adask_gram_ex(dv.ctx().handle, dv.dtype_code(A.dtype), A.data_ptr(), n, d, A.stride(0),
+                                        float(nu2), None if lam is None else lam.data_ptr(), dv.dtype_code(dv.F64),
+                                        H.data_ptr(), d, dv.stream()), "gram")
     return H
 
 

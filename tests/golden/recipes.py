@@ -48,3 +48,81 @@ def run_instance(i: int):
     b = A.T @ (A @ r.standard_normal(d) + 0.01 * r.standard_normal(n))
     lam = np.random.default_rng(123).uniform(1, 10, d) if lam_u else np.ones(d)
     return A, b, lam
+
+
+# ---------------------------------------------------------------- BASELINE configs
+# (config index, n) of the solve-level parity fixtures: configs 1-2 at full
+# size, configs 3-4 at n/16 (SURVEY.md 7 hard part 9; the fp64 reference
+# cannot hold their full-size A in host memory).  T = accepted iterations to
+# the config's target, from the reference's own tracked run.
+BASELINE_N = {1: 1 << 16, 2: 1 << 20, 3: 1 << 17, 4: 1 << 20}
+BLOCK4 = 1 << 17  # block rows of the config-4 block SRHT at n/16 (8 blocks)
+T_MAX = {1: 16, 2: 14, 3: 12, 4: 12}  # tracked-run length; T* is read off its trace
+
+
+def baseline_instance(cfg_index: int, n: int):
+    """The BASELINE.json recipe at n rows, numpy on the host:
+    G = N(0,1)/sqrt(n), V = qr(N(0,1)).Q, A = G diag(sigma) V^T, x0, eps,
+    b = A^T (A x0 + 0.01 eps), Lam = I or default_rng(123).uniform(1, 10).
+    A is cast to the config's dtype (fp32 for configs 3-4: the reference
+    then runs on float64 of that same fp32 matrix, problem.py:51).  The GEMM
+    for A is thread-count independent in OpenBLAS; the GEMVs for b are not,
+    so they run on one thread (the fixture stores fingerprints of both)."""
+    from threadpoolctl import threadpool_limits
+
+    from paper_2104_14101_b200.configs import CONFIGS
+
+    cfg = CONFIGS[cfg_index]
+    d = cfg.d
+    rng = np.random.default_rng(0)
+    G = rng.standard_normal((n, d))
+    G /= np.sqrt(n)
+    V, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    x0 = rng.standard_normal(d)
+    eps = rng.standard_normal(n)
+    A = G @ (cfg.sigma()[:, None] * V.T)
+    del G
+    if cfg.dtype == "float32":
+        A = A.astype(np.float32)
+    with threadpool_limits(limits=1, user_api="blas"):
+        A64 = A.astype(np.float64, copy=False)
+        b = A64.T @ (A64 @ x0 + 0.01 * eps)
+    del A64
+    lam = np.random.default_rng(123).uniform(1.0, 10.0, d) if cfg.lam_uniform else np.ones(d)
+    return A, b, lam
+
+
+def fingerprint(a: np.ndarray) -> np.ndarray:
+    """Column sums in fp64 plus a CRC of the bytes: lets a test tell whether
+    the instance it rebuilt is bitwise the one the fixture was made on."""
+    import zlib
+
+    a = np.ascontiguousarray(a)
+    return np.array([float(zlib.crc32(memoryview(a).cast("B")))] + list(
+        np.asarray(a, dtype=np.float64).reshape(a.shape[0], -1).sum(axis=0)[:8]))
+
+
+# ---------------------------------------------------------------- fixed-sketch solvers
+# (solver, family, n, d, c, m, rho, seed, T, tol, s)
+FIXED_RUNS = [("ihs", "srht", 3000, 40, 1, 400, 0.25, 3, 8, 0.0, 1),
+              ("pcg", "sjlt", 5000, 64, 2, 512, 0.0, 5, 10, 0.0, 1),
+              ("pcg", "srht", 2048, 32, 1, 128, 0.0, 9, 30, 1e-8, 1),
+              ("polyak", "srht", 4096, 50, 1, 500, 0.1, 4, 10, 0.0, 1),
+              ("cg", "", 2000, 60, 1, 0, 0.0, 0, 25, 0.0, 1),
+              ("ihs", "sjlt", 1000, 20, 1, 100, 0.3, 6, 6, 0.0, 3),
+              ("polyak", "sjlt", 6000, 48, 2, 600, 0.2, 8, 8, 0.0, 1)]
+
+
+def fixed_instance(i: int):
+    solver, fam, n, d, c, m, rho, seed, T, tol, s = FIXED_RUNS[i]
+    r = np.random.default_rng(7000 + i)
+    G = r.standard_normal((n, d)) / np.sqrt(n)
+    V, _ = np.linalg.qr(r.standard_normal((d, d)))
+    sig = 0.93 ** np.arange(1, d + 1, dtype=float)
+    A = (G * sig[None, :]) @ V.T
+    X0 = r.standard_normal((d, c))
+    B = A.T @ (A @ X0 + 0.01 * r.standard_normal((n, c)))
+    if c == 1:
+        B = B[:, 0]
+    lam = r.uniform(1, 4, d)
+    return A, B, lam, 0.05
