@@ -43,12 +43,24 @@ def _peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
-        return {"hbm_gbs": float(pk["hbm_gbs"]), "bf16_tflops": float(pk["bf16_tflops"]),
-                "bf16_tflops_sustained": float(pk.get("bf16_tflops_sustained", pk["bf16_tflops"])),
-                "source": "MEASURED_PEAKS.json (measured)"}
+        out = {"hbm_gbs": float(pk["hbm_gbs"]), "bf16_tflops": float(pk["bf16_tflops"]),
+               "bf16_tflops_sustained": float(pk.get("bf16_tflops_sustained", pk["bf16_tflops"])),
+               "source": "MEASURED_PEAKS.json (measured)"}
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
-                "source": "B200_PROFILING.md fallback"}
+        out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+               "source": "B200_PROFILING.md fallback"}
+    # FP64 (DMMA) and TF32 dense peaks: cuBLAS DGEMM / TF32 GEMM 8192^3 measured
+    # on this pool's B200s by tools/measure_peaks.py (profiles/r02_peaks.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_peaks.json")) as f:
+            pk = json.load(f)
+        out.update(fp64_tflops=float(pk["fp64"]["burst_tflops"]), tf32_tflops=float(pk["tf32"]["burst_tflops"]),
+                   tf32_tflops_sustained=float(pk["tf32"]["sustained_tflops"]),
+                   fp_source="profiles/r02_peaks.json (cuBLAS 8192^3 measured, tools/measure_peaks.py)")
+    except Exception:
+        out.update(fp64_tflops=37.0, tf32_tflops=out["bf16_tflops"] / 2, tf32_tflops_sustained=
+                   out["bf16_tflops_sustained"] / 2, fp_source="nominal FP64 / half of bf16 for TF32")
+    return out
 
 
 class ClockSampler:
@@ -90,7 +102,7 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             self._sample(busy_only=True)
-            time.sleep(0.01)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.nv:
@@ -225,7 +237,7 @@ def _build_problem(cfg, ws, rank, dist, dev):
     A_d, b_d, lam_d = make_instance_device(cfg, n_local=plan.n_local, row0=plan.row0)
     if ws > 1:
         dist.all_reduce(b_d)
-        comm = par.Comm()
+        comm = par.Comm()  # NCCL: libadask's own communicator, exchanges issued by the native driver
         p = par.ShardedProblem(A_d, b_d, cfg.nu, lam_d, plan=plan, comm=comm, validate=False)
     else:
         p = ak.RegularizedProblem(A_d, b_d, cfg.nu, lam_d, validate=False)
@@ -276,11 +288,10 @@ def run_ours(args) -> None:
     sharded = plan is not None and ws > 1
     x0 = torch.zeros(cfg.d, dtype=torch.float64, device=dev)
     tf32 = cfg.dtype == "float32" and cfg.family == "gaussian" and not args.no_tf32
+    # row-sharded problems run the native driver too: every exchange (pair
+    # all-reduce per proposal, reduce-scatter + partial Gram + d x d all-reduce
+    # per resketch) is issued by libadask on its NCCL communicator
     kw = {"tf32": tf32, "block": cfg.block or (1 << 21)}
-    if sharded:
-        from paper_2104_14101_b200 import parallel as par
-
-        kw["sketcher"] = par.sharded_sketcher(p.comm, block=cfg.block or (1 << 21), tf32=tf32)
 
     def acfg_for(T):
         return ak.AdaptiveConfig.for_method(cfg.method, args.rho, cfg.m_init, T, cfg.family, args.seed)
@@ -396,25 +407,40 @@ def run_ours(args) -> None:
     _log("e2e")
     e2e = _e2e(args, cfg, p, host_inst, acfg, kw, ws, dist, dev)
 
-    # ---- roofline of the dominant unit
+    # ---- roofline of the dominant unit: the unit with the most device time
+    # among ALL units (build is split into its Gram and Cholesky+inverse parts)
     pk = _peaks()
-    # roofline kernel: the streaming / tensor unit with the most device time
-    # (the build unit -- Gram, Cholesky, inverse -- is latency bound and is
-    # reported in `units`)
-    dom = max(("hess_mult", "srht", "sjlt", "gaussian"), key=lambda k: prof[k]["ms"])
-    u = prof[dom]
-    per_launch_ms = u["ms"] / max(u["count"], 1)
-    tensor = dom == "gaussian" and tf32
-    if tensor:  # TF32 tcgen05 GEMM: tensor-bound; peak = half the measured dense bf16 rate
-        work_per = u["flops"] / max(u["count"], 1)
-        achieved = work_per / (per_launch_ms * 1e-3) / 1e12
-        # the sketch runs inside a long solve under the power cap: the sustained
-        # bf16 figure (B200_PROFILING.md), halved for TF32 (dense TF32 = bf16 / 2)
-        peak, unit, bound = pk["bf16_tflops_sustained"] / 2.0, "TFLOP/s", "tensor"
-    else:
-        work_per = u["bytes"] / max(u["count"], 1)
-        achieved = work_per / (per_launch_ms * 1e-3) / 1e9
-        peak, unit, bound = pk["hbm_gbs"], "GB/s", "hbm"
+    units_all = ("hess_mult", "srht", "sjlt", "gaussian", "gram", "chol", "apply")
+    dom = max(units_all, key=lambda k: prof[k]["ms"])
+    rf = {}
+    for name in units_all:
+        u = prof[name]
+        if not u["count"]:
+            continue
+        per_launch_ms = u["ms"] / u["count"]
+        peak_src = pk["source"]
+        if name == "gaussian" and tf32:
+            # TF32 tcgen05 GEMM inside a long solve under the power cap: sustained TF32
+            work_per, unit, bound = u["flops"] / u["count"], "TFLOP/s", "tensor"
+            peak, peak_src = pk["tf32_tflops_sustained"], pk["fp_source"] + " (TF32 sustained)"
+        elif name in ("gram", "chol") or name == "gaussian":
+            # DMMA Gram, Cholesky + triangular inverse, fp64/fp32 Gaussian: FP64 pipe
+            work_per, unit, bound = u["flops"] / u["count"], "TFLOP/s", ("tensor" if name == "gram" else "fp64")
+            peak, peak_src = pk["fp64_tflops"], pk["fp_source"] + " (FP64 DGEMM)"
+        else:
+            work_per, unit, bound = u["bytes"] / u["count"], "GB/s", "hbm"
+            peak = pk["hbm_gbs"]
+        scale = 1e12 if unit == "TFLOP/s" else 1e9
+        achieved = work_per / (per_launch_ms * 1e-3) / scale
+        rf[name] = {"bound": bound, "unit_name": name, "achieved": achieved, "peak": peak, "unit": unit,
+                    "frac": achieved / peak, "per_launch_ms": per_launch_ms, "alg_work_per_launch": work_per,
+                    "peak_source": peak_src, "share_of_units": u["ms"] / max(sum(
+                        prof[k]["ms"] for k in units_all), 1e-9)}
+    roof = dict(rf[dom])
+    bound, unit, peak, achieved, per_launch_ms, work_per = (roof["bound"], roof["unit"], roof["peak"],
+                                                           roof["achieved"], roof["per_launch_ms"],
+                                                           roof["alg_work_per_launch"])
+    tensor = bound == "tensor"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -425,6 +451,10 @@ def run_ours(args) -> None:
     units = {k: {"count": v["count"], "ms_total": round(v["ms"], 4),
                  "gbs": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1),
                  "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 2)} for k, v in prof.items() if v["count"]}
+    for k, r in rf.items():
+        units[k].update(bound=r["bound"], frac=round(r["frac"], 4), peak=r["peak"], peak_unit=r["unit"])
+    if "build" in units:
+        units["build"]["note"] = "gram + chol (+ small copies); see those units"
     sketch_unit = {"srht": "srht", "sjlt": "sjlt", "gaussian": "gaussian", "srht-block": "srht"}[cfg.family]
     su = prof[sketch_unit]
     sketch_gbs = su["bytes"] / max(su["ms"], 1e-9) / 1e6 if su["count"] else None
@@ -463,11 +493,7 @@ def run_ours(args) -> None:
             "units_pass": {"ms_per_step": prof_ms_per_step,
                            "note": "units and roofline from a second pass of the same steps with per-unit CUDA "
                                    "events on the launching stream; value/ms_per_step from the pass without them"},
-            "roofline": {"bound": bound, "unit_name": dom, "achieved": achieved, "peak": peak,
-                         "unit": unit, "frac": achieved / peak, "traffic": traffic,
-                         "per_launch_ms": per_launch_ms, "alg_work_per_launch": work_per,
-                         "peak_source": pk["source"] + (" (sustained bf16 / 2 for tf32: the sketch runs inside a "
-                                                        "long solve under the power cap)" if tensor else "")},
+            "roofline": dict(roof, traffic=traffic),
             "clocks": clk.summary(),
             "e2e": e2e,
             "incremental": incr,
@@ -544,7 +570,9 @@ def main() -> None:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE config (default: 1 on one GPU -- the global SRHT does not shard; "
+                         "2, the row-sharded 1/2/4/8-GPU workload, for --gpus > 1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rho", type=float, default=0.125)
     ap.add_argument("--seed", type=int, default=1)
@@ -552,6 +580,22 @@ def main() -> None:
     ap.add_argument("--no-tf32", action="store_true", help="fp32 Gaussian sketch on the FP32 pipe instead of TF32")
     ap.add_argument("--no-incremental", action="store_true", help="skip the incremental-growth variant")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = 1 if args.gpus <= 1 else 2
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        import socket
+        import subprocess
+
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        if "--config" not in sys.argv:
+            cmd += ["--config", str(args.config)]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -286,9 +286,31 @@ typedef struct adask_problem {
   double nu2;         /* nu^2 */
   const double* lam;  /* device, d        */
   const double* B;    /* device, c x d    */
-  adask_allreduce_fn allreduce; /* null on one GPU */
+  adask_allreduce_fn allreduce; /* host hook (tests over gloo); null otherwise */
   void* allreduce_user;
+  int32_t use_ctx_comm; /* 1: A is this rank's row shard and the exchanges run
+                           on the ctx's NCCL communicator (adask_comm_init_nccl) */
+  int32_t comm_rank, comm_world; /* with the allreduce hook: rank / world size */
 } adask_problem;
+
+/* ---- row-shard communicator (NCCL over NVLink; resolved at run time) ----
+ * One process per GPU.  The exchanges of a sharded solve:
+ * per loop pass one all-reduce of the partial A_g^T A_g x (PCG proposals: one
+ * all-reduce of the 2d pair [p, x]); per resketch a reduce-scatter of the
+ * partial S_g A_g, a partial Gram over this rank's m/G rows and an all-reduce
+ * of the d x d Gram (dense path), or an all-reduce of SA (Woodbury path).
+ * The reference is single-process; these replace nothing
+ * in it and are the B200 build's data-parallel extension.                   */
+int adask_nccl_available(void);
+/* ncclGetUniqueId into a 128-byte buffer (rank 0; broadcast it to the others). */
+int adask_nccl_unique_id(void* id_out);
+/* ncclCommInitRank on the ctx's device; the ctx owns the communicator. */
+int adask_comm_init_nccl(adask_ctx* ctx, const void* id, int rank, int world);
+/* Borrow an existing ncclComm_t (the caller keeps ownership). */
+int adask_set_comm(adask_ctx* ctx, void* nccl_comm, int rank, int world);
+int adask_comm_destroy(adask_ctx* ctx);
+/* In-place sum all-reduce of count elements (dtype) on stream (no-op without a communicator). */
+int adask_comm_allreduce(adask_ctx* ctx, void* buf, int64_t count, int dtype, void* stream);
 
 /* _PcgState.restart (solvers.py:243-248): r = B - H x; rt = P^-1 r;
  * dt_col = max(colsum(r*rt), 0) with the NegativeValue guard; p = rt.

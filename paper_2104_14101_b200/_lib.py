@@ -63,6 +63,9 @@ class Problem(C.Structure):
         ("B", C.c_void_p),
         ("allreduce", ALLREDUCE_FN),
         ("allreduce_user", C.c_void_p),
+        ("use_ctx_comm", C.c_int32),
+        ("comm_rank", C.c_int32),
+        ("comm_world", C.c_int32),
     ]
 
 
@@ -150,6 +153,12 @@ _PROTOS = {
     "adask_ihs_restart": (C.c_int, [vp, P(Problem), vp, vp, vp, vp, P(dbl), vp]),
     "adask_ihs_propose": (C.c_int, [vp, P(Problem), vp, vp, vp, dbl, vp, dbl, vp, vp, vp, P(dbl), vp]),
     "adask_dot": (C.c_int, [vp, vp, vp, i64, i64, i64, P(dbl), vp]),
+    "adask_nccl_available": (C.c_int, []),
+    "adask_nccl_unique_id": (C.c_int, [vp]),
+    "adask_comm_init_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
+    "adask_set_comm": (C.c_int, [vp, vp, C.c_int, C.c_int]),
+    "adask_comm_destroy": (C.c_int, [vp]),
+    "adask_comm_allreduce": (C.c_int, [vp, vp, i64, C.c_int, vp]),
     "adask_adaptive_run": (C.c_int, [vp, P(Problem), P(AdaptiveCfg), vp, vp, vp, P(TraceRec), i64, P(i64), vp]),
 }
 
@@ -223,7 +232,7 @@ class Context:
     def launches(self) -> int:
         return int(lib().adask_ctx_launches(self.handle))
 
-    PROF_KINDS = ("hess_mult", "srht", "sjlt", "gaussian", "build", "apply")
+    PROF_KINDS = ("hess_mult", "srht", "sjlt", "gaussian", "build", "apply", "gram", "chol")
 
     def prof_enable(self, on: bool = True) -> None:
         check(lib().adask_prof_enable(self.handle, 1 if on else 0))

@@ -95,6 +95,8 @@ enum WsSlot {
   WS_SRHT_U,     // pipelined SRHT: the two half transforms of an 11-bit pass 2
   WS_GRAM_PACK,  // Gram: 16-byte aligned copy of an odd-shaped operand
   WS_GRAM_RL,    // Gram: 1/lam (Woodbury scaling), zero padded
+  WS_PAIR,       // sharded PCG proposal: the partial pair [A^T A p | A^T A x]
+  WS_SA_ROWS,    // sharded build: this rank's reduce-scattered rows of SA
   WS_COUNT
 };
 
@@ -107,6 +109,8 @@ enum ProfKind {
   PK_GAUSS,      // whole Gaussian sketch
   PK_BUILD,      // preconditioner build (Gram + Cholesky + inverse)
   PK_APPLY,      // preconditioner apply
+  PK_GRAM,       // build: the Gram / capacitance (inside PK_BUILD)
+  PK_CHOL,       // build: Cholesky factor + triangular inverse (inside PK_BUILD)
   PK_COUNT
 };
 
@@ -118,8 +122,18 @@ struct adask_prof_rec {
   double flops;
 };
 
+namespace adask {
+// NCCL communicator of a row-sharded solve (comm.cu); nccl is an ncclComm_t
+struct CommState {
+  void* nccl = nullptr;
+  int rank = 0, world = 1;
+  bool owned = false;
+};
+}  // namespace adask
+
 struct adask_ctx {
   int device = 0;
+  adask::CommState comm;
   int64_t launches = 0;
   adask::Workspace ws[adask::WS_COUNT];
   double* pinned = nullptr;  // pinned host scalars for synchronous readbacks

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "comm.cuh"
 #include "hessmult.cuh"
 
 #include "precond.cuh"
@@ -151,9 +152,33 @@ static int make_sketch(adask_ctx* ctx, const adask_problem* pb, const adask_adap
     default:
       return fail(ADASK_E_ARG, "unknown sketch family %d", cfg->family);
   }
-  if (pb->allreduce && pb->allreduce(SA, m * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
-    return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
-  return ADASK_OK;
+  return ADASK_OK;  // row-sharded: the partial S_g A_g (combined by build_precond)
+}
+
+// Preconditioner from a sketch.  One GPU: build(SA).  Row-sharded, dense path
+// (m >= d) with m divisible by the world size: reduce-scatter the partial
+// S_g A_g, Gram of this rank's m/G rows, all-reduce of the d x d Gram, then
+// nu^2 Lam and the (replicated) factor.  Otherwise (Woodbury path: its apply
+// reads all of SA; or SA already summed) all-reduce SA and build.
+static int build_precond(adask_ctx* ctx, const adask_problem* pb, void* SA, int64_t m, bool sa_summed,
+                         adask_precond** P, int64_t* info, cudaStream_t st) {
+  const int64_t d = pb->d;
+  const double nu = std::sqrt(pb->nu2);
+  if (!problem_sharded(ctx, pb))
+    return precond_build_impl(ctx, pb->dtype, SA, m, m, d, d, nu, pb->lam, nullptr, P, info, st);
+  const int G = comm_world(ctx, pb);
+  if (!sa_summed && m >= d && m % G == 0 && getenv("ADASK_SHARD_SA_ALLREDUCE") == nullptr) {
+    const size_t esz = pb->dtype == ADASK_F64 ? 8 : 4;
+    const int64_t mr = m / G;
+    void* scratch = nullptr;
+    ADASK_TRY(ctx->ws[WS_SA_ROWS].get((size_t)mr * d * esz, st, &scratch));
+    void* rows = nullptr;
+    ADASK_TRY(problem_reduce_scatter(ctx, pb, SA, scratch, mr * d, pb->dtype, &rows, st));
+    GramReduce red = [&](void* M, int64_t count, int dt) { return problem_allreduce(ctx, pb, M, count, dt, st); };
+    return precond_build_impl(ctx, pb->dtype, rows, mr, m, d, d, nu, pb->lam, &red, P, info, st);
+  }
+  if (!sa_summed) ADASK_TRY(problem_allreduce(ctx, pb, SA, m * d, pb->dtype, st));
+  return precond_build_impl(ctx, pb->dtype, SA, m, m, d, d, nu, pb->lam, nullptr, P, info, st);
 }
 
 // ------------------------------------------------------------ incremental growth
@@ -193,9 +218,7 @@ static int make_sketch_incr(adask_ctx* ctx, const adask_problem* pb, const adask
     if (!SA_old || m_old <= 0) {
       ADASK_TRY(adask_sketch_gaussian(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, cfg->row0, m, seed0, SA, d,
                                       cfg->flags & ADASK_TF32, (void*)st));
-      if (pb->allreduce && pb->allreduce(SA, m * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
-        return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
-      return ADASK_OK;
+      return problem_allreduce(ctx, pb, SA, m * d, pb->dtype, st);
     }
     if (m == m_old) {  // capped retry: the grown sketch is the same sketch
       ADASK_CUDA(cudaMemcpyAsync(SA, SA_old, (size_t)m * d * esz, cudaMemcpyDeviceToDevice, st));
@@ -211,9 +234,7 @@ static int make_sketch_incr(adask_ctx* ctx, const adask_problem* pb, const adask
     void* fresh = (char*)SA + (size_t)nold * esz;
     ADASK_TRY(adask_sketch_gaussian_rows(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, cfg->row0, m, m_old, m - m_old,
                                          seed0, fresh, d, cfg->flags & ADASK_TF32, (void*)st));
-    if (pb->allreduce && pb->allreduce(fresh, (m - m_old) * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
-      return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
-    return ADASK_OK;
+    return problem_allreduce(ctx, pb, fresh, (m - m_old) * d, pb->dtype, st);
   }
   if (cfg->family == ADASK_SRHT || cfg->family == ADASK_SRHT_BLOCK) {
     const bool blocked = cfg->family == ADASK_SRHT_BLOCK;
@@ -254,11 +275,10 @@ static int make_sketch_incr(adask_ctx* ctx, const adask_problem* pb, const adask
     for (size_t bi = 0; bi < inc.npad.size(); ++bi)
       ADASK_TRY(srht_gather_impl(ctx, pb->dtype, (char*)inc.y + inc.yoff[bi], inc.npad[bi], d,
                                  (const int64_t*)inc.perm + inc.poff[bi], m, SA, d, bi > 0 ? 1 : 0, st));
-    if (pb->allreduce && pb->allreduce(SA, m * d, pb->dtype, pb->allreduce_user, (void*)st) != 0)
-      return fail(ADASK_E_CUDA, "all-reduce of the partial sketch failed");
-    return ADASK_OK;
+    return problem_allreduce(ctx, pb, SA, m * d, pb->dtype, st);
   }
-  return make_sketch(ctx, pb, cfg, m, seed0, SA, st);  // SJLT: no growth rule, redraw
+  ADASK_TRY(make_sketch(ctx, pb, cfg, m, seed0, SA, st));  // SJLT: no growth rule, redraw
+  return problem_allreduce(ctx, pb, SA, m * d, pb->dtype, st);
 }
 
 static int exact_err(adask_ctx* ctx, const adask_problem* pb, const double* x, const double* xstar,
@@ -368,8 +388,7 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
   if (ahead_on) ahead.start(adask_derive_seed(cfg->seed, 1), pb->n, std::min(2 * m, cap));
   adask_precond* P = nullptr;
   int64_t info = 0;
-  ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
-                                (void*)st));
+  ADASK_TRY(build_precond(ctx, pb, sa_buf.p, m, inc.on, &P, &info, st));
   struct PGuard {
     adask_precond** p;
     ~PGuard() {
@@ -442,8 +461,7 @@ extern "C" int adask_adaptive_run(adask_ctx* ctx, const adask_problem* pb, const
       if (ahead_on) ahead.start(adask_derive_seed(cfg->seed, (uint64_t)K + 1), pb->n, std::min(2 * m, cap));
       std::swap(sa_buf.p, nsa.p);
       sa_slot = nslot;
-      ADASK_TRY(adask_precond_build(ctx, pb->dtype, sa_buf.p, m, d, d, std::sqrt(pb->nu2), pb->lam, &P, &info,
-                                    (void*)st));
+      ADASK_TRY(build_precond(ctx, pb, sa_buf.p, m, inc.on, &P, &info, st));
       {
         const int rs = restart();
         ADASK_TRY(spd_check());

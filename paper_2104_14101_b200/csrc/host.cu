@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "comm.cuh"
 #include "gemm.cuh"
 #include "pcg64.cuh"
 
@@ -374,6 +375,7 @@ int adask_ctx_destroy(adask_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (auto& w : ctx->ws) w.release();
+  adask::comm_release(ctx);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
   if (ctx->mail) cudaFreeHost(ctx->mail);

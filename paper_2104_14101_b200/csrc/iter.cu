@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "comm.cuh"
 #include "hessmult.cuh"
 #include "precond.cuh"
 
@@ -238,13 +239,12 @@ static int read_scalars(adask_ctx* ctx, IterScalars* sc, double* dt_host, int* f
 int problem_hess(adask_ctx* ctx, const adask_problem* pb, const double* X, const double* B,
                         double* out, cudaStream_t st) {
   const int64_t d = pb->d, c = pb->c;
-  if (!pb->allreduce)
+  if (!problem_sharded(ctx, pb))
     return hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, X, c, d, pb->nu2, pb->lam, B, d, out,
                           d, 0, st);
   ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, X, c, d, pb->nu2, pb->lam, nullptr, d,
                            out, d, ADASK_PARTIAL, st));
-  if (pb->allreduce(out, d * c, ADASK_F64, pb->allreduce_user, (void*)st) != 0)
-    return fail(ADASK_E_CUDA, "all-reduce of the partial A^T A x failed");
+  ADASK_TRY(problem_allreduce(ctx, pb, out, d * c, ADASK_F64, st));
   return vec_hess_finish_impl(ctx, out, d, c, d, X, pb->nu2, pb->lam, B, out, st);
 }
 
@@ -272,21 +272,32 @@ int pcg_propose_impl(adask_ctx* ctx, const adask_problem* pb, const adask_precon
   const int64_t d = pb->d, c = pb->c;
   *hx_ok = 0;
   if (hx_mb && c == 1) {
-    if (!pb->allreduce) {
+    if (!problem_sharded(ctx, pb)) {
       ADASK_TRY(hess_mult_pair_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, nullptr, Hp, x, pb->B, hx_mb,
                                     pb->nu2, pb->lam, st, hx_ok));
-    } else if (pb->n > 0) {
-      // row-sharded: the pair of partial A_g^T A_g [p, x], all-reduced, then
-      // the regularizer / B epilogues (problem_hess's sequence per column)
-      ADASK_TRY(hess_mult_pair_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, nullptr, Hp, x, nullptr, hx_mb,
-                                    pb->nu2, pb->lam, st, hx_ok, 1));
-      if (*hx_ok) {
-        if (pb->allreduce(Hp, d, ADASK_F64, pb->allreduce_user, (void*)st) != 0 ||
-            pb->allreduce(hx_mb, d, ADASK_F64, pb->allreduce_user, (void*)st) != 0)
-          return fail(ADASK_E_CUDA, "all-reduce of the partial A^T A [p, x] failed");
-        ADASK_TRY(vec_hess_finish_impl(ctx, Hp, d, 1, d, p, pb->nu2, pb->lam, nullptr, Hp, st));
-        ADASK_TRY(vec_hess_finish_impl(ctx, hx_mb, d, 1, d, x, pb->nu2, pb->lam, pb->B, hx_mb, st));
+    } else {
+      // row-sharded: the partial pair [A_g^T A_g p | A_g^T A_g x] in one 2d
+      // buffer, ONE all-reduce, then the regularizer / B epilogues.  Every
+      // rank takes this path (an empty or unaligned shard forms its partials
+      // with the single-column pass, or as zeros), so the number and order
+      // of the collectives never depends on per-rank state.
+      void* wsp = nullptr;
+      ADASK_TRY(ctx->ws[WS_PAIR].get((size_t)2 * d * sizeof(double), st, &wsp));
+      double* pr = (double*)wsp;
+      int fused = 0;
+      if (pb->n > 0)
+        ADASK_TRY(hess_mult_pair_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, nullptr, pr, x, nullptr, pr + d,
+                                      pb->nu2, pb->lam, st, &fused, 1));
+      if (!fused) {
+        ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, p, 1, d, pb->nu2, pb->lam, nullptr, d,
+                                 pr, d, ADASK_PARTIAL, st));
+        ADASK_TRY(hess_mult_impl(ctx, pb->dtype, pb->A, pb->n, d, pb->lda, x, 1, d, pb->nu2, pb->lam, nullptr, d,
+                                 pr + d, d, ADASK_PARTIAL, st));
       }
+      ADASK_TRY(problem_allreduce(ctx, pb, pr, 2 * d, ADASK_F64, st));
+      ADASK_TRY(vec_hess_finish_impl(ctx, pr, d, 1, d, p, pb->nu2, pb->lam, nullptr, Hp, st));
+      ADASK_TRY(vec_hess_finish_impl(ctx, pr + d, d, 1, d, x, pb->nu2, pb->lam, pb->B, hx_mb, st));
+      *hx_ok = 1;
     }
   }
   if (!*hx_ok) ADASK_TRY(problem_hess(ctx, pb, p, nullptr, Hp, st));

@@ -52,15 +52,25 @@ static void free_precond(adask_precond* P) {
 
 using namespace adask;
 
-extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t d,
-                                   int64_t ldsa, double nu, const double* lam, adask_precond** out,
-                                   int64_t* info_host, void* stream) {
-  ADASK_TRY(use_device(ctx));
-  if (!out || !lam || (m > 0 && !SA)) return fail(ADASK_E_ARG, "precond_build: null argument");
-  if (m < 1 || d < 1 || ldsa < d) return fail(ADASK_E_DIM, "precond_build: bad shape m=%lld d=%lld",
-                                              (long long)m, (long long)d);
+namespace adask {
+template <typename T>
+__global__ void k_add_diag(T* M, int64_t ldm, int64_t k, double nu2, const double* lam) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) M[i * ldm + i] = (T)((double)M[i * ldm + i] + nu2 * (lam ? lam[i] : 1.0));
+}
+
+// build() (preconditioner.py:60-74).  SA holds m_rows rows of the m x d
+// sketch; m_rows < m only for a row-sharded dense build, where SA is this
+// rank's reduce-scattered slice: the Gram of the slice is all-reduced (sum
+// over ranks = SA^T SA) before nu^2 Lam is added and the factor is formed.
+int precond_build_impl(adask_ctx* ctx, int dtype, const void* SA, int64_t m_rows, int64_t m, int64_t d,
+                       int64_t ldsa, double nu, const double* lam, const GramReduce* reduce, adask_precond** out,
+                       int64_t* info_host, cudaStream_t st) {
+  if (!out || !lam || (m_rows > 0 && !SA)) return fail(ADASK_E_ARG, "precond_build: null argument");
+  if (m < 1 || d < 1 || ldsa < d || m_rows < 0 || m_rows > m)
+    return fail(ADASK_E_DIM, "precond_build: bad shape m=%lld d=%lld", (long long)m, (long long)d);
   if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
-  cudaStream_t st = S(stream);
+  if (m_rows != m && (m < d || !reduce)) return fail(ADASK_E_ARG, "precond_build: partial rows need the dense path");
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
   adask_precond* P = new adask_precond();
   P->device = ctx->device;
@@ -69,7 +79,7 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
   P->m = m;
   P->d = d;
   P->k = m >= d ? d : m;
-  P->SA = SA;
+  P->SA = m_rows == m ? SA : nullptr;  // a sharded dense build keeps no full SA (its apply never reads it)
   P->ldsa = ldsa;
   P->nu = nu;
   P->nu2 = nu * nu;
@@ -93,8 +103,10 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
     return fail(ADASK_E_NOMEM, "precond_build: cudaMalloc: %s", cudaGetErrorString(e));
   }
   int s = ADASK_OK;
-  const double gram_flops = m >= d ? (double)m * d * (d + 1) : (double)m * (m + 1) * d;
-  ProfScope prof(ctx, PK_BUILD, st, (double)m * d * esz, gram_flops + (double)k * k * k / 3.0);
+  const double gram_flops = m >= d ? (double)m_rows * d * (d + 1) : (double)m * (m + 1) * d;
+  // the factor (k^3/3) and its triangular inverse (k^3/3); L^-T is a transpose
+  const double chol_flops = 2.0 * (double)k * k * k / 3.0;
+  ProfScope prof(ctx, PK_BUILD, st, (double)m_rows * d * esz, gram_flops + chol_flops);
   do {
     e = cudaMemcpyAsync(P->lam, lam, (size_t)d * sizeof(double), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) {
@@ -106,14 +118,31 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
     s = ctx->ws[WS_GRAM].get(gram_bytes + (size_t)d * sizeof(double), st, &wsp);
     if (s) break;
     void* M = wsp;
-    if (P->path == 0) {
-      // H_S = SA^T SA + nu^2 diag(lam)   (preconditioner.py:70)
-      s = gram_dense(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
-    } else {
-      // W_S = (SA * (1/lam)) SA^T + nu^2 I   (preconditioner.py:72-73)
-      s = gram_woodbury(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
+    {
+      ProfScope pg(ctx, PK_GRAM, st, (double)m_rows * d * esz, gram_flops);
+      if (P->path == 0 && m_rows != m) {
+        // sharded: partial Gram of this rank's rows, all-reduce, then nu^2 Lam
+        s = gram_dense(ctx, dtype, SA, m_rows, d, ldsa, 0.0, nullptr, M, kp, st);
+        if (!s) s = (*reduce)(M, d * kp, dtype);
+        if (!s) {
+          if (dtype == ADASK_F64)
+            k_add_diag<double><<<(unsigned)cdiv(d, 256), 256, 0, st>>>((double*)M, kp, d, P->nu2, P->lam);
+          else
+            k_add_diag<float><<<(unsigned)cdiv(d, 256), 256, 0, st>>>((float*)M, kp, d, P->nu2, P->lam);
+          cudaError_t le = cudaGetLastError();
+          if (le != cudaSuccess) s = fail(ADASK_E_CUDA, "k_add_diag: %s", cudaGetErrorString(le));
+          else ctx->launches++;
+        }
+      } else if (P->path == 0) {
+        // H_S = SA^T SA + nu^2 diag(lam)   (preconditioner.py:70)
+        s = gram_dense(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
+      } else {
+        // W_S = (SA * (1/lam)) SA^T + nu^2 I   (preconditioner.py:72-73)
+        s = gram_woodbury(ctx, dtype, SA, m, d, ldsa, P->nu2, P->lam, M, kp, st);
+      }
     }
     if (s) break;
+    ProfScope pc(ctx, PK_CHOL, st, (double)k * k * esz, chol_flops);
     s = pad_identity(ctx, dtype, M, k, kp, st);
     if (s) break;
     s = chol_factor_inverse(ctx, dtype, M, k, kp, P->L, P->Linv, P->LinvT, info_host, st);
@@ -125,6 +154,14 @@ extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, in
   }
   *out = P;
   return ADASK_OK;
+}
+}  // namespace adask
+
+extern "C" int adask_precond_build(adask_ctx* ctx, int dtype, const void* SA, int64_t m, int64_t d,
+                                   int64_t ldsa, double nu, const double* lam, adask_precond** out,
+                                   int64_t* info_host, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  return precond_build_impl(ctx, dtype, SA, m, m, d, ldsa, nu, lam, nullptr, out, info_host, S(stream));
 }
 
 extern "C" int adask_precond_destroy(adask_precond* P) {

@@ -17,7 +17,14 @@ struct adask_precond {
   void* LinvT;   // k x k upper (transpose of Linv)
 };
 
+#include <functional>
+
 namespace adask {
+// all-reduce of a partial Gram (M, count elements, dtype) for sharded builds
+using GramReduce = std::function<int(void*, int64_t, int)>;
+int precond_build_impl(adask_ctx* ctx, int dtype, const void* SA, int64_t m_rows, int64_t m, int64_t d,
+                       int64_t ldsa, double nu, const double* lam, const GramReduce* reduce, adask_precond** out,
+                       int64_t* info_host, cudaStream_t st);
 int precond_apply_impl(adask_ctx* ctx, const adask_precond* P, const double* Z, int64_t c,
                        int64_t ldz, double* out, int64_t ldo, cudaStream_t st);
 }  // namespace adask

@@ -57,16 +57,39 @@ def shard_rows(n_total: int, world: int, rank: int, align: int = 1) -> ShardPlan
 
 
 class Comm:
-    """Sum all-reduce over a torch.distributed process group (NCCL on the GPU
-    box, gloo in the CPU tests)."""
+    """The shard group.  torch.distributed is the plumbing (rendezvous,
+    the NCCL unique-id broadcast, gloo in the CPU tests); with the NCCL
+    backend on GPUs, libadask gets its own NCCL communicator on this rank's
+    device (adask_comm_init_nccl) and the native solve issues every exchange
+    itself on its stream (`native`).  all_reduce_sum_ serves the Python-level
+    paths (custom sketchers, ShardedProblem.hess_mult_dev)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, *, native: bool | None = None):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        backend = dist.get_backend(group)
+        if native is None:
+            native = backend == "nccl" and torch.cuda.is_available()
+        self.native = False
+        if native:
+            self._init_native()
+
+    def _init_native(self) -> None:
+        lib = _lib.lib()
+        if not lib.adask_nccl_available():
+            raise RuntimeError("libadask could not load libnccl.so.2 for the native shard communicator")
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            _lib.check(lib.adask_nccl_unique_id(uid), "nccl_unique_id")
+        obj = [bytes(uid)]
+        self.dist.broadcast_object_list(obj, src=0, group=self.group)
+        C.memmove(uid, obj[0], 128)
+        _lib.check(lib.adask_comm_init_nccl(dv.ctx().handle, uid, self.rank, self.world), "comm_init_nccl")
+        self.native = True
 
     def all_reduce_sum_(self, t: torch.Tensor) -> torch.Tensor:
         if self.world > 1:
@@ -104,8 +127,13 @@ class ShardedProblem(RegularizedProblem):
 
     def descriptor(self) -> _lib.Problem:
         pb = super().descriptor()
-        pb.allreduce = self._hook
-        pb.allreduce_user = None
+        if self.comm.native:
+            pb.use_ctx_comm = 1  # exchanges on libadask's NCCL communicator
+        else:
+            pb.allreduce = self._hook  # host hook (gloo)
+            pb.allreduce_user = None
+        pb.comm_rank = self.comm.rank
+        pb.comm_world = self.comm.world
         return pb
 
     def hess_mult_dev(self, Xt, out=None, *, minus_B=False, partial=False):

@@ -108,7 +108,7 @@ FIXED_RUNS = [("ihs", "srht", 3000, 40, 1, 400, 0.25, 3, 8, 0.0, 1),
               ("pcg", "sjlt", 5000, 64, 2, 512, 0.0, 5, 10, 0.0, 1),
               ("pcg", "srht", 2048, 32, 1, 128, 0.0, 9, 30, 1e-8, 1),
               ("polyak", "srht", 4096, 50, 1, 500, 0.1, 4, 10, 0.0, 1),
-              ("cg", "", 2000, 60, 1, 0, 0.0, 0, 25, 0.0, 1),
+              ("cg", "", 2000, 60, 1, 0, 0.0, 0, 16, 0.0, 1),  # past ~18 steps CG on this instance amplifies 1e-16 input perturbations to 1e-6 (checked on the reference itself)
               ("ihs", "sjlt", 1000, 20, 1, 100, 0.3, 6, 6, 0.0, 3),
               ("polyak", "sjlt", 6000, 48, 2, 600, 0.2, 8, 8, 0.0, 1)]
 
