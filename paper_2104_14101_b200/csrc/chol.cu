@@ -60,9 +60,37 @@ int pad_identity(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, cuda
   return ADASK_OK;
 }
 
+int chol_df_launch(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, void* L, void* Li, void* LiT,
+                   int* info, cudaStream_t st);
+
+static int chol_finish(adask_ctx* ctx, int* info, int64_t* info_host, cudaStream_t st) {
+  if (ctx->defer_spd) {
+    // the driver reads pinned_flags[1] after its next synchronization
+    ADASK_CUDA(cudaMemcpyAsync(ctx->pinned_flags + 1, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (info_host) *info_host = 0;
+    return ADASK_OK;
+  }
+  ADASK_CUDA(cudaMemcpyAsync(ctx->pinned_flags, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  ADASK_CUDA(cudaStreamSynchronize(st));
+  const int h = ctx->pinned_flags[0];
+  if (info_host) *info_host = h;
+  if (h != 0) return fail(ADASK_E_NOT_SPD, "Matrix is not positive definite (leading minor %d)", h);
+  return ADASK_OK;
+}
+
 int chol_factor_inverse(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, void* L, void* Li,
                         void* LiT, int64_t* info_host, cudaStream_t st) {
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  if (!getenv("ADASK_CHOL_OLD")) {
+    // dataflow kernel (chol_df.cu): writes every tile of L, Li, LiT itself
+    if (kp % 32 || kp < k) return fail(ADASK_E_ARG, "chol: bad padding");
+    void* wsp = nullptr;
+    ADASK_TRY(ctx->ws[WS_CHOL].get(256, st, &wsp));
+    int* info = (int*)wsp;
+    ADASK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
+    ADASK_TRY(chol_df_launch(ctx, dtype, M, k, kp, L, Li, LiT, info, st));
+    return chol_finish(ctx, info, info_host, st);
+  }
   // tile edge: 32 unless overridden (ADASK_CHOL_NB=64)
   int nb = 32;
   if (const char* e = getenv("ADASK_CHOL_NB")) nb = atoi(e) == 64 ? 64 : 32;

@@ -95,6 +95,7 @@ enum WsSlot {
   WS_SRHT_U,     // pipelined SRHT: the two half transforms of an 11-bit pass 2
   WS_GRAM_PACK,  // Gram: 16-byte aligned copy of an odd-shaped operand
   WS_GRAM_RL,    // Gram: 1/lam (Woodbury scaling), zero padded
+  WS_CHOL_FLAGS, // dataflow Cholesky: ticket counter + per-tile flags
   WS_PAIR,       // sharded PCG proposal: the partial pair [A^T A p | A^T A x]
   WS_SA_ROWS,    // sharded build: this rank's reduce-scattered rows of SA
   WS_COUNT
@@ -134,6 +135,10 @@ struct CommState {
 struct adask_ctx {
   int device = 0;
   adask::CommState comm;
+  // dataflow Cholesky (chol_df.cu): flag block identity, epoch, ticket base
+  void* chol_flags_ptr = nullptr;
+  int chol_epoch = 0;
+  unsigned chol_ticket = 0;
   int64_t launches = 0;
   adask::Workspace ws[adask::WS_COUNT];
   double* pinned = nullptr;  // pinned host scalars for synchronous readbacks

@@ -249,7 +249,7 @@ int problem_hess(adask_ctx* ctx, const adask_problem* pb, const double* X, const
 }
 
 static int check_problem(const adask_problem* pb) {
-  if (!pb || !pb->A || pb->n < 0 || pb->d < 1 || pb->c < 1 || pb->lda < pb->d || !pb->lam)
+  if (!pb || (!pb->A && pb->n > 0) || pb->n < 0 || pb->d < 1 || pb->c < 1 || pb->lda < pb->d || !pb->lam)
     return fail(ADASK_E_ARG, "bad problem descriptor");
   return ADASK_OK;
 }
