@@ -96,6 +96,7 @@ enum WsSlot {
   WS_GRAM_PACK,  // Gram: 16-byte aligned copy of an odd-shaped operand
   WS_GRAM_RL,    // Gram: 1/lam (Woodbury scaling), zero padded
   WS_CHOL_FLAGS, // dataflow Cholesky: ticket counter + per-tile flags
+  WS_CHOL_ITEMS, // dataflow Cholesky: helper item list (per nblk)
   WS_PAIR,       // sharded PCG proposal: the partial pair [A^T A p | A^T A x]
   WS_SA_ROWS,    // sharded build: this rank's reduce-scattered rows of SA
   WS_COUNT
@@ -139,6 +140,7 @@ struct adask_ctx {
   void* chol_flags_ptr = nullptr;
   int chol_epoch = 0;
   unsigned chol_ticket = 0;
+  int chol_items_nb = -1, chol_nitems = 0;
   int64_t launches = 0;
   adask::Workspace ws[adask::WS_COUNT];
   double* pinned = nullptr;  // pinned host scalars for synchronous readbacks
