@@ -39,10 +39,15 @@ def test_adsk1_errors(tmp_path):
 def test_cli_flag_errors_exit_2(tmp_path):
     assert cli.main(["solve", "--data", str(tmp_path), "--solver", "nope", "--out", "x.csv"]) == 2
     with pytest.raises(Exception):
-        cli._check_flags("cg", {"m": 5, "m_init": None, "rho": None, "sketch": None, "s": None})
-    assert cli._check_flags("ada-pcg", {"m": None, "m_init": None, "rho": None, "sketch": None, "s": None}) == \
+        cli.resolve_options("cg", {"m": 5, "m_init": None, "rho": None, "sketch": None, "s": None})
+    with pytest.raises(Exception):
+        cli.resolve_options("pcg", {"m": None, "m_init": None, "rho": None, "sketch": None, "s": None})
+    assert cli.resolve_options("ada-pcg", {"m": None, "m_init": None, "rho": None, "sketch": None, "s": None}) == \
         {"m": None, "m_init": 1, "rho": 0.125, "sketch": "gaussian", "s": 1}
-    assert cli._parse_m("3d", 10) == 30
+    assert cli.parse_sketch_size("3d", 10) == 30
+    assert cli.parse_run("ada-pcg:srht:m_init=16", 10) == \
+        ("ada-pcg", {"m": None, "m_init": 16, "rho": 0.125, "sketch": "srht", "s": 1})
+    assert cli.main(["solve", "--data", str(tmp_path), "--solver", "cg", "--nu", "-1", "--out", "x.csv"]) == 2
 
 
 def test_cli_missing_data_exit_3(tmp_path):
