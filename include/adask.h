@@ -169,6 +169,12 @@ int adask_sketch_gaussian_rows(adask_ctx* ctx, int dtype, const void* A, int64_t
                                int64_t lda, int64_t row0, int64_t m_total, int64_t k0, int64_t mk,
                                uint64_t key, void* SA, int64_t ldsa, uint32_t flags, void* stream);
 
+/* SA = S A for an explicit m x n sketch matrix S (device): the Gaussian
+ * sketch with the reference's own numpy draw (embeddings.py:71-73), for the
+ * opt-in bitwise-randomness mode; the default Gaussian path is Philox.     */
+int adask_sketch_dense(adask_ctx* ctx, int dtype, const void* S, int64_t m, int64_t n, int64_t lds,
+                       const void* A, int64_t d, int64_t lda, void* SA, int64_t ldsa, void* stream);
+
 /* SRHT: SA = Y[idx] * sqrt(n_pad/m), Y = fwht(diag(signs) A_padded)/sqrt(n_pad)
  * (embeddings.py:81-102, linalg.py:62-88).  `g` is the fresh generator of
  * the sketch seed; signs are draws [0, n), idx = choice(n_pad, m) after them.

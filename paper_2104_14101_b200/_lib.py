@@ -129,6 +129,7 @@ _PROTOS = {
     "adask_philox_gaussian_host": (C.c_int, [i64, i64, i64, u64, vp, i64]),
     "adask_sketch_gaussian": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, i64, i64, u64, vp, i64, u32, vp]),
     "adask_sketch_gaussian_rows": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, i64, i64, i64, i64, u64, vp, i64, C.c_uint32, vp]),
+    "adask_sketch_dense": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, vp, i64, i64, vp, i64, vp]),
     "adask_sketch_srht": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, P(PCG64State), i64, vp, i64, P(i64), u32, vp]),
     "adask_sketch_sjlt": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, i64, i64, i64, i64, P(PCG64State),
                                     P(i64), u64, vp, i64, u32, vp]),

@@ -70,3 +70,24 @@ extern "C" int adask_sketch_gaussian(adask_ctx* ctx, int dtype, const void* A, i
                          (long long)m);
   return adask_sketch_gaussian_rows(ctx, dtype, A, n_local, d, lda, row0, m, 0, m, key, SA, ldsa, flags, stream);
 }
+
+// SA = S A for an explicit m x n sketch matrix S (device, row-major, lds):
+// the Gaussian sketch with the reference's own draw (numpy ziggurat normals
+// of default_rng(seed), embeddings.py:71-72, generated on the host by the
+// caller) when bitwise-equal randomness to the reference is wanted (the
+// opt-in rng="numpy" mode of embeddings.set_gaussian_rng).
+extern "C" int adask_sketch_dense(adask_ctx* ctx, int dtype, const void* Smat, int64_t m, int64_t n, int64_t lds,
+                                  const void* A, int64_t d, int64_t lda, void* SA, int64_t ldsa, void* stream) {
+  ADASK_TRY(use_device(ctx));
+  if (m < 1 || n < 0 || d < 1 || lds < n || lda < d || ldsa < d) return fail(ADASK_E_DIM, "sketch_dense: bad shape");
+  if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
+  cudaStream_t st = S(stream);
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  ProfScope prof(ctx, PK_GAUSS, st, (double)n * d * esz, 2.0 * (double)m * n * d);
+  if (n == 0) {
+    ADASK_CUDA(cudaMemset2DAsync(SA, ldsa * esz, 0, d * esz, m, st));
+    return ADASK_OK;
+  }
+  return gemm_impl(ctx, dtype, m, d, n, 1.0, Smat, lds, false, A, lda, false, nullptr, 0.0, SA, ldsa, 0.0, nullptr,
+                   false, st);
+}

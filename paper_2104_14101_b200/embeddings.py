@@ -107,11 +107,48 @@ def _result(SA: torch.Tensor, spec: SketchSpec, n: int, like) -> SketchedData:
 
 
 # ----------------------------------------------------------------- device cores
+_GAUSSIAN_RNG = "philox"
+
+
+def set_gaussian_rng(mode: str) -> str:
+    """Select the Gaussian sketch's randomness; returns the previous mode.
+
+    "philox" (default): S is generated on the device from Philox4x32-10
+    keyed by (seed, sketch row, global A row) -- the product's definition,
+    shard-invariant, never materialized on the host.
+    "numpy": S is the reference's own draw, default_rng(seed).standard_normal
+    ((m, n)) / sqrt(m) (embeddings.py:71-72), generated on the host and
+    applied on the GPU (adask_sketch_dense) -- for running the reference's
+    seed-pinned tests unchanged.  Forces the Python driver loop."""
+    global _GAUSSIAN_RNG
+    if mode not in ("philox", "numpy"):
+        raise ValueError(f"unknown Gaussian rng mode {mode!r}")
+    prev, _GAUSSIAN_RNG = _GAUSSIAN_RNG, mode
+    return prev
+
+
+def gaussian_rng() -> str:
+    return _GAUSSIAN_RNG
+
+
+def _gaussian_numpy_dev(Ad: torch.Tensor, m: int, seed: int) -> torch.Tensor:
+    n, d = Ad.shape
+    S = np.random.default_rng(seed).standard_normal((m, n)) / np.sqrt(m)
+    Sd = torch.from_numpy(S).to(device=Ad.device, dtype=Ad.dtype)
+    SA = torch.empty((m, d), dtype=Ad.dtype, device=Ad.device)
+    _lib.check(_lib.lib().adask_sketch_dense(dv.ctx().handle, dv.dtype_code(Ad.dtype), Sd.data_ptr(), m, n,
+                                             Sd.stride(0), Ad.data_ptr(), d, Ad.stride(0), SA.data_ptr(),
+                                             SA.stride(0), dv.stream()), "sketch_dense")
+    return SA
+
+
 def gaussian_dev(Ad: torch.Tensor, m: int, seed: int, *, row0: int = 0, tf32: bool = False,
                  out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
     n, d = Ad.shape
     _check_m(m, n)
     m = int(m)
+    if _GAUSSIAN_RNG == "numpy" and row0 == 0 and out is None and not accumulate:
+        return _gaussian_numpy_dev(Ad, m, seed)
     SA = out if out is not None else torch.empty((m, d), dtype=Ad.dtype, device=Ad.device)
     flags = (_lib.ACCUMULATE if accumulate else 0) | (_lib.TF32 if tf32 else 0)
     key = int(seed) & 0xFFFFFFFFFFFFFFFF

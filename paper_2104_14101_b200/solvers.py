@@ -23,7 +23,7 @@ import torch
 
 from . import _lib
 from . import device as dv
-from .embeddings import SketchSpec, derive_seed, padded_rows, sketch_dev
+from .embeddings import SketchSpec, derive_seed, gaussian_rng, padded_rows, sketch_dev
 from .errors import BreakdownDetected
 from .preconditioner import Preconditioner, build_dev
 from .problem import ExactSolution, RegularizedProblem, exact_error_dev
@@ -481,6 +481,7 @@ def adaptive_run(p: RegularizedProblem, x0, cfg: AdaptiveConfig, method: str = "
         raise ValueError("method 'polyak' is experimental; pass experimental=True")
     if native is None:
         native = (sketcher is None and method != "polyak" and 0 <= int(cfg.seed) < 2**64
+                  and not (cfg.family == "gaussian" and gaussian_rng() == "numpy")
                   and cfg.family in _FAMILY_CODE and os.environ.get("ADASK_PY_DRIVER") != "1")
     if incremental:
         if sketcher is not None or method == "polyak":
