@@ -259,7 +259,7 @@ def _exact_solution(ak, p, cfg, sharded, dist):
         return ak.direct_solve(p)
     from paper_2104_14101_b200.problem import gram_fp64
 
-    H = gram_fp64(p.A)
+    H = gram_fp64(p.A_dev)
     dist.all_reduce(H)
     H.diagonal().add_(p.nu**2 * p.lam_dev)
     L = ak.cholesky(H)
@@ -465,7 +465,7 @@ def run_ours(args) -> None:
         from oracle import adasketch_oracle as O
 
         _log("cpu baseline")
-        A_s, b_s, lam_s, scale, sample = _host_sample(cfg, None if cfg.index < 2 else p.A)
+        A_s, b_s, lam_s, scale, sample = _host_sample(cfg, None if cfg.index < 2 else p.A_dev)
         t0 = time.perf_counter()
         _oracle_solve(O, cfg, A_s, b_s, lam_s, t_star, args.rho, args.seed)
         cpu_s = (time.perf_counter() - t0) * scale
@@ -483,7 +483,7 @@ def run_ours(args) -> None:
                        "parallelism": (f"replicas{ws}" if cfg.index < 2 else f"rowshard{ws}") if ws > 1
                        else "single",
                        "l2": "A (%.0f MiB per GPU) exceeds the 126 MB L2; no flush" % (
-                           p.A.numel() * p.A.element_size() / 2**20)},
+                           p.A_dev.numel() * p.A_dev.element_size() / 2**20)},
             "rel_err_final": rel_err,
             "step_ms": step_ms,
             "schedule": trace.schedule(),
@@ -521,13 +521,13 @@ def _e2e(args, cfg, p, host_inst, acfg, kw, ws, dist, dev):
         try:
             import psutil
 
-            need = p.A.numel() * p.A.element_size()
+            need = p.A_dev.numel() * p.A_dev.element_size()
             if psutil.virtual_memory().available < 1.5 * need:
                 return {"value": None, "unit": "s", "skipped": f"host RAM < 1.5 x {need >> 30} GiB for pinned A"}
         except Exception:
             pass
-        A_pin = torch.empty(p.A.shape, dtype=p.A.dtype, pin_memory=True)
-        A_pin.copy_(p.A)
+        A_pin = torch.empty(p.A_dev.shape, dtype=p.A_dev.dtype, pin_memory=True)
+        A_pin.copy_(p.A_dev)
         b_pin = p.Bt[0].cpu().pin_memory()
         lam_pin = p.lam_dev.cpu().pin_memory()
     x0_pin = torch.zeros(cfg.d, dtype=torch.float64).pin_memory()

@@ -187,8 +187,34 @@ def lib():
                         continue
                     fn.restype = res
                     fn.argtypes = args
-                _lib = h
+                _lib = _Serialized(h)
     return _lib
+
+
+_call_lock = threading.RLock()
+
+
+class _Serialized:
+    """libadask with every entry point serialized by one re-entrant lock.
+    The device context (workspaces, pinned scalars, the order of its stream)
+    is shared by all host threads of the process -- the reference CLI's
+    `compare`, for one, runs its solver jobs on a thread pool -- while the C
+    ABI allows one caller per context at a time (include/adask.h)."""
+
+    def __init__(self, h):
+        self._h = h
+
+    def __getattr__(self, name):
+        fn = getattr(self._h, name)
+        if not name.startswith("adask_"):
+            return fn
+
+        def call(*args, _fn=fn):
+            with _call_lock:
+                return _fn(*args)
+
+        setattr(self, name, call)
+        return call
 
 
 def exported_symbols() -> list[str]:

@@ -117,7 +117,7 @@ class ShardedProblem(RegularizedProblem):
 
         def _hook(ptr, count, dtype, user, stream):
             try:
-                t = torch.as_tensor(_CudaView(int(ptr), int(count), int(dtype)), device=self.A.device)
+                t = torch.as_tensor(_CudaView(int(ptr), int(count), int(dtype)), device=self.A_dev.device)
                 self.comm.all_reduce_sum_(t)
                 return 0
             except Exception:  # reported through the C status path
@@ -156,7 +156,7 @@ def sharded_sketcher(comm: Comm, *, block: int = 1 << 21, tf32: bool = False):
     sketch with global randomness, then all-reduce."""
 
     def sk(p: RegularizedProblem, spec: SketchSpec) -> torch.Tensor:
-        A = p.A
+        A = p.A_dev
         if spec.family == "sjlt":
             SA = sjlt_dev(A, spec.m, spec.seed, spec.s, row0=p.row0, n_total=p.n_total)
         elif spec.family == "gaussian":
@@ -188,6 +188,6 @@ def block_srht_sketcher(block: int = 1 << 21):
     derive_seed(seed, b)) over fixed row blocks, summed in block order."""
 
     def sk(p: RegularizedProblem, spec: SketchSpec) -> torch.Tensor:
-        return _block_srht_local(p.A, spec.m, spec.seed, p.row0, block)
+        return _block_srht_local(p.A_dev, spec.m, spec.seed, p.row0, block)
 
     return sk

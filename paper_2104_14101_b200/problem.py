@@ -40,10 +40,11 @@ class RegularizedProblem:
         t = dv.resolve_dtype(dtype) if dtype is not None else (
             A.dtype if isinstance(A, torch.Tensor) and A.dtype in (dv.F64, dv.F32) else dv.F64)
         self._like = A
-        self.A = dv.to_device(A, t)
-        if self.A.dim() != 2:
-            raise DimensionMismatch(f"A must be 2-D, got shape {tuple(self.A.shape)}")
-        n, d = self.A.shape
+        self._A_host = A if isinstance(A, np.ndarray) and A.dtype == np.float64 and A.ndim == 2 else None
+        self.A_dev = dv.to_device(A, t)
+        if self.A_dev.dim() != 2:
+            raise DimensionMismatch(f"A must be 2-D, got shape {tuple(self.A_dev.shape)}")
+        n, d = self.A_dev.shape
         Bd = dv.to_device(B, dv.F64)
         if Bd.dim() == 1:
             Bd = Bd[:, None]
@@ -53,26 +54,37 @@ class RegularizedProblem:
         self.nu = float(nu)
         if not np.isfinite(self.nu) or self.nu <= 0:
             raise ValueError(f"nu must be positive and finite, got {self.nu}")
-        lam_d = torch.ones(d, dtype=dv.F64, device=self.A.device) if lam is None else dv.to_device(lam, dv.F64)
+        lam_d = torch.ones(d, dtype=dv.F64, device=self.A_dev.device) if lam is None else dv.to_device(lam, dv.F64)
         if tuple(lam_d.shape) != (d,):
             raise DimensionMismatch(f"lam must have shape ({d},), got {tuple(lam_d.shape)}")
         self.lam_dev = lam_d.contiguous()
         if validate:
             if not bool(torch.isfinite(self.lam_dev).all()) or float(self.lam_dev.min()) < 1.0:
                 raise ValueError("lam entries must be finite and >= 1")
-            if not (_all_finite(self.A) and bool(torch.isfinite(self.Bt).all())):
+            if not (_all_finite(self.A_dev) and bool(torch.isfinite(self.Bt).all())):
                 raise ValueError("A and B must be finite")
         self.row0 = int(row0)
         self.n_total = n if n_total is None else int(n_total)
 
     # ---- reference properties
     @property
+    def A(self):
+        """The data matrix like the caller passed it: numpy float64 for a
+        numpy input (the reference's cast, problem.py:51), else the device
+        tensor.  The solvers use A_dev."""
+        if isinstance(self._like, torch.Tensor):
+            return self.A_dev
+        if self._A_host is None:
+            self._A_host = dv.to_host_like(self.A_dev, self._like)
+        return self._A_host
+
+    @property
     def n(self) -> int:
-        return self.A.shape[0]
+        return self.A_dev.shape[0]
 
     @property
     def d(self) -> int:
-        return self.A.shape[1]
+        return self.A_dev.shape[1]
 
     @property
     def c(self) -> int:
@@ -88,14 +100,14 @@ class RegularizedProblem:
 
     @property
     def dtype(self) -> torch.dtype:
-        return self.A.dtype
+        return self.A_dev.dtype
 
     def descriptor(self) -> _lib.Problem:
         pb = _lib.Problem()
-        pb.dtype = dv.dtype_code(self.A.dtype)
-        pb.A = self.A.data_ptr()
-        pb.n, pb.d = self.A.shape
-        pb.lda = self.A.stride(0)
+        pb.dtype = dv.dtype_code(self.A_dev.dtype)
+        pb.A = self.A_dev.data_ptr()
+        pb.n, pb.d = self.A_dev.shape
+        pb.lda = self.A_dev.stride(0)
         pb.c = self.c
         pb.nu2 = self.nu**2
         pb.lam = self.lam_dev.data_ptr()
@@ -111,8 +123,8 @@ class RegularizedProblem:
             raise DimensionMismatch(f"iterate has {d} rows, expected {self.d}")
         out = torch.empty_like(Xt) if out is None else out
         B = self.Bt if minus_B else None
-        _lib.check(_lib.lib().adask_hess_mult(dv.ctx().handle, dv.dtype_code(self.A.dtype), self.A.data_ptr(),
-                                              self.n, d, self.A.stride(0), Xt.data_ptr(), c, d,
+        _lib.check(_lib.lib().adask_hess_mult(dv.ctx().handle, dv.dtype_code(self.A_dev.dtype), self.A_dev.data_ptr(),
+                                              self.n, d, self.A_dev.stride(0), Xt.data_ptr(), c, d,
                                               self.nu**2, self.lam_dev.data_ptr(),
                                               None if B is None else B.data_ptr(), d, out.data_ptr(), d,
                                               _lib.PARTIAL if partial else 0, dv.stream()),
@@ -137,7 +149,7 @@ class RegularizedProblem:
         """Dense d x d Hessian (problem.py:109-111)."""
         from .preconditioner import gram_dev
 
-        return dv.to_host_like(gram_dev(self.A, self.nu**2, self.lam_dev), self._like)
+        return dv.to_host_like(gram_dev(self.A_dev, self.nu**2, self.lam_dev), self._like)
 
 
 @dataclass
@@ -170,11 +182,11 @@ def direct_solve(p: RegularizedProblem) -> ExactSolution:
 
     if p.n < p.d:
         raise DimensionMismatch("direct_solve needs n >= d on the device path")
-    if p.A.dtype == dv.F64:
-        P = build_dev(p.A, p.nu, p.lam_dev)
+    if p.A_dev.dtype == dv.F64:
+        P = build_dev(p.A_dev, p.nu, p.lam_dev)
         X = P.solve_dev(p.Bt)
         return ExactSolution(x_star=dv.to_host_like(X.t().contiguous(), p._like))
-    H = gram_fp64(p.A, p.nu**2, p.lam_dev)
+    H = gram_fp64(p.A_dev, p.nu**2, p.lam_dev)
     L = cholesky(H)
     Y = tri_solve(L, p.Bt.t().contiguous())
     X = tri_solve(L, Y, transposed=True)

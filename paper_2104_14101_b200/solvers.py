@@ -233,7 +233,7 @@ class _PolyakState(_IhsState):
 
 # ------------------------------------------------------------ fixed sketch
 def _fixed_sketch_setup(p: RegularizedProblem, m, family, seed, s, tf32=False):
-    SA = sketch_dev(p.A, SketchSpec(family, m, seed, s=s), tf32=tf32)
+    SA = sketch_dev(p.A_dev, SketchSpec(family, m, seed, s=s), tf32=tf32)
     return build_dev(SA, p.nu, p.lam_dev)
 
 
@@ -315,7 +315,7 @@ def cg(p, x0, T, tol=0.0, sol=None):
     iterations or once that value falls to tol."""
     clock = _Clock()
     Xt, vec = _promote(p, x0)
-    P = build_dev(torch.zeros((1, p.d), dtype=p.A.dtype, device=Xt.device), 1.0,
+    P = build_dev(torch.zeros((1, p.d), dtype=p.A_dev.dtype, device=Xt.device), 1.0,
                   torch.ones(p.d, dtype=dv.F64, device=Xt.device))
     trace = SolverTrace()
     sol_t = _sol_cols(sol)
@@ -423,7 +423,7 @@ def _adaptive_sketch(p: RegularizedProblem, cfg: AdaptiveConfig, m: int, K: int,
     spec = SketchSpec(cfg.family, m, derive_seed(cfg.seed, K), s=cfg.s)
     if sketcher is not None:
         return sketcher(p, spec)
-    return sketch_dev(p.A, spec, tf32=tf32)
+    return sketch_dev(p.A_dev, spec, tf32=tf32)
 
 
 _FAMILY_CODE = {"gaussian": 0, "srht": 1, "sjlt": 2, "srht-block": 3}

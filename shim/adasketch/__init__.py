@@ -71,6 +71,11 @@ for _m in [_ref] + [sys.modules["_adasketch_ref." + s] for s in _SUBS]:
     for _name, _obj in HOT_PATH.items():
         if hasattr(_m, _name):
             setattr(_m, _name, _obj)
+    # tuples of exception classes built at import time (e.g. the CLI's
+    # exit-code groups) must hold the classes the GPU code raises
+    for _name, _val in list(vars(_m).items()):
+        if isinstance(_val, tuple) and _val and all(isinstance(c, type) for c in _val):
+            setattr(_m, _name, tuple(HOT_PATH.get(c.__name__, c) for c in _val))
 
 sys.modules["adasketch"] = _ref
 for _s in _SUBS:
