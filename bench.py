@@ -140,7 +140,7 @@ def _cfg(idx: int):
 SAMPLE_ROWS = {0: None, 1: None, 2: 1 << 14, 3: 1 << 15, 4: 1 << 18}
 
 
-def _host_sample(cfg, A_dev=None):
+def _host_sample(cfg, A_dev=None, p_dev=None):
     """Host (numpy fp64) instance for the CPU arms.  Configs 0-1: the full
     instance (numpy recipe).  Configs 2-4 (16-64 GB): the first SAMPLE_ROWS
     rows of the device instance with b recomputed for that sample; the CPU
@@ -153,6 +153,13 @@ def _host_sample(cfg, A_dev=None):
         A, b, lam = make_instance(cfg)
         return A.astype(np.float64), b, lam, 1.0, f"full instance n={cfg.n}"
     import torch
+
+    if cfg.index == 2 and A_dev is not None and p_dev is not None:
+        # config 2 (16 GiB fp64): the full instance the GPU solved, copied to
+        # the host -- one full-size oracle solve, no extrapolation
+        As = A_dev.cpu().numpy()
+        return (As, p_dev.Bt[0].cpu().numpy(), p_dev.lam_dev.cpu().numpy(), 1.0,
+                f"full instance n={cfg.n} (the device instance, copied to the host)")
 
     from paper_2104_14101_b200.configs import make_instance_device
 
@@ -465,7 +472,7 @@ def run_ours(args) -> None:
         from oracle import adasketch_oracle as O
 
         _log("cpu baseline")
-        A_s, b_s, lam_s, scale, sample = _host_sample(cfg, None if cfg.index < 2 else p.A_dev)
+        A_s, b_s, lam_s, scale, sample = _host_sample(cfg, None if cfg.index < 2 else p.A_dev, p)
         t0 = time.perf_counter()
         _oracle_solve(O, cfg, A_s, b_s, lam_s, t_star, args.rho, args.seed)
         cpu_s = (time.perf_counter() - t0) * scale

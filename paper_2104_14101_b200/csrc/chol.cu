@@ -158,7 +158,7 @@ extern "C" int adask_cholesky(adask_ctx* ctx, int dtype, const void* M, int64_t 
   if (dtype != ADASK_F64 && dtype != ADASK_F32) return fail(ADASK_E_ARG, "bad dtype");
   cudaStream_t st = S(stream);
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
-  const int64_t kp = cdiv(k, 64) * 64;
+  const int64_t kp = cdiv(k, getenv("ADASK_CHOL_NB") ? 64 : 32) * (getenv("ADASK_CHOL_NB") ? 64 : 32);
   const size_t mat = (size_t)kp * kp * esz;
   char* work = nullptr;
   ADASK_CUDA(cudaMallocAsync((void**)&work, 4 * mat, st));

@@ -84,7 +84,8 @@ int precond_build_impl(adask_ctx* ctx, int dtype, const void* SA, int64_t m_rows
   P->nu = nu;
   P->nu2 = nu * nu;
   const int64_t k = P->k;
-  const int64_t kp = cdiv(k, 64) * 64;
+  // padded to the dataflow Cholesky's 32-row tiles (64 for the round-1 kernel's NB = 64 variant)
+  const int64_t kp = cdiv(k, getenv("ADASK_CHOL_NB") ? 64 : 32) * (getenv("ADASK_CHOL_NB") ? 64 : 32);
   P->kp = kp;
   P->stream = st;
   const size_t lam_bytes = align_up((size_t)d * sizeof(double), 256);
