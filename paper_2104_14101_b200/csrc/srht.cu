@@ -442,10 +442,13 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   if (ilog2(n_pad) > 24) return fail(ADASK_E_ARG, "sketch_srht: n_pad > 2^24 unsupported");
   static const bool htrace = getenv("ADASK_HOST_TRACE") != nullptr;
   const auto h0 = std::chrono::steady_clock::now();
-  ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4), 0.0, true);
-  // signs: draws [0, n) of integers(0, 2)
+  // signs: draws [0, n) of integers(0, 2).  The workspace is fetched before
+  // the (gated) unit window opens: a growing Workspace::get synchronizes the
+  // stream, which would wait on the gate kernel (the plan / Z workspaces of
+  // fwht_select are grown by the bench's warm-up solves before any profiled one)
   void* sw = nullptr;
   ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(1ll << ilog2(n), 32) * 4 + 64, st, &sw));  // padded: bulk-copied per tile
+  ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4), 0.0, true);
   uint32_t* sgn = (uint32_t*)sw;
   ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
   // idx = choice(n_pad, m, replace=False) after the n sign draws (host)
