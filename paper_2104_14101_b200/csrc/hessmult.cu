@@ -175,7 +175,17 @@ __global__ void __launch_bounds__(288, 1) k_hess_tma(const T* __restrict__ A, in
     }
     fence_barrier_init();
   }
-  __syncthreads();
+  // A^T A 0 = 0 exactly: an all-zero right-hand side (the solvers' usual
+  // x0 = 0 at the first restart) writes zero partials without streaming A
+  bool nz = false;
+  for (int64_t j = tid; j < d; j += blockDim.x) nz |= (x0[j] != 0.0) || (NX == 2 && x1[j] != 0.0);
+  if (!__syncthreads_or(nz)) {
+    for (int q = 0; q < NX; ++q) {
+      double* out = (q == 0 ? part0 : part1) + (int64_t)blockIdx.x * d;
+      for (int64_t j = tid; j < d; j += blockDim.x) out[j] = 0.0;
+    }
+    return;
+  }
   if (warp == NW) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();

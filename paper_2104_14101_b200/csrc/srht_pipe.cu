@@ -629,6 +629,12 @@ int fwht_pipe_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int64
   return 1;
 }
 
+int fwht_pipe_group(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const uint32_t* sgn,
+                    int64_t n_pad, int64_t m, void* out, int64_t ldo, double c1, double c2, int accumulate,
+                    cudaStream_t st, int hybrid, bool selected, bool comb, int64_t nslots, int64_t zrows, int64_t B,
+                    int64_t G, int b1, int L2, int L2p, const int32_t* d_plan, const int32_t* d_map2,
+                    const int32_t* d_rep, void* zw, int64_t ldz, void* uw);
+
 int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                      const uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out, int64_t ldo,
                      double c1, double c2, int accumulate, cudaStream_t st, int hybrid) {
@@ -703,12 +709,49 @@ int fwht_select_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
     else
       ADASK_TRY(fwht_build_map2(ctx, d_plan + B, m, d_map2, map_rows, st));
   }
+  // Column groups: when the intermediate Z of all d columns would exceed the
+  // L2 budget, the two passes run group by group over column panels so that
+  // a group's Z (nslots * G rows x its columns) is written by pass 1 and read
+  // back by pass 2 while it is still L2-resident, instead of a round trip
+  // through HBM (config 1 at m >= 512: Z is as large as A).  Every column is
+  // transformed independently, so the result is bitwise the one-group result.
+  // Off by default: measured at 2^16 x 1024 fp64 (tools/srht_bench.py), 2-16
+  // groups of separate launches cost more in per-launch setup and wave tails
+  // than the HBM round trip of Z they save (m = 4096: 357 us in one group,
+  // 391-617 us in groups) -- the L2-resident schedule needs both passes in
+  // one persistent kernel.
+  static const int64_t zbudget =
+      getenv("ADASK_SRHT_ZBUDGET_MB") ? (atoll(getenv("ADASK_SRHT_ZBUDGET_MB")) << 20) : INT64_MAX;
+  const int64_t panel = 64 / (int64_t)esz;  // columns per 64-byte tile row
+  int64_t gw = d;
+  if ((int64_t)zrows * (int64_t)align_up((size_t)d, 16 / esz) * (int64_t)esz > zbudget) {
+    gw = std::max<int64_t>(panel, zbudget / ((int64_t)zrows * (int64_t)esz) / panel * panel);
+    gw = std::min<int64_t>(gw, d);
+  }
   void* zw = nullptr;
-  const int64_t ldz = (int64_t)align_up((size_t)d, 16 / esz);
+  const int64_t ldz = (int64_t)align_up((size_t)gw, 16 / esz);
   ADASK_TRY(ctx->ws[WS_SRHT].get((size_t)zrows * ldz * esz, st, &zw));
   void* uw = nullptr;
   if (comb) ADASK_TRY(ctx->ws[WS_SRHT_U].get((size_t)2 * m * ldz * esz, st, &uw));
+  for (int64_t c0 = 0; c0 < d; c0 += gw) {
+    const int64_t w = std::min<int64_t>(gw, d - c0);
+    ADASK_TRY(fwht_pipe_group(ctx, dtype, (const char*)A + c0 * esz, n, w, lda, sgn, n_pad, m, (char*)out + c0 * esz,
+                              ldo, c1, c2, accumulate, st, hybrid, idx != nullptr, comb, nslots, zrows, B, G, b1, L2,
+                              L2p, d_plan, d_map2, d_rep, zw, (int64_t)align_up((size_t)w, 16 / esz), uw));
+  }
+  return ADASK_OK;
+}
 
+// one column group of fwht_select_pipe: pass 1 over A's columns [c0, c0 + d)
+// into Z (row pitch ldz), pass 2 from Z into the same columns of out
+int fwht_pipe_group(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const uint32_t* sgn,
+                    int64_t n_pad, int64_t m, void* out, int64_t ldo, double c1, double c2, int accumulate,
+                    cudaStream_t st, int hybrid, bool selected, bool comb, int64_t nslots, int64_t zrows, int64_t B,
+                    int64_t G, int b1, int L2, int L2p, const int32_t* d_plan, const int32_t* d_map2,
+                    const int32_t* d_rep, void* zw, int64_t ldz, void* uw) {
+  (void)B;
+  (void)selected;
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
   PipeArgs a{};
   a.d = d;
   a.nslots = (int)nslots;
