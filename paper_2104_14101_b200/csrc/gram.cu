@@ -340,7 +340,8 @@ int run(adask_ctx* ctx, Args a, cudaStream_t st) {
   ADASK_CUDA(launch_pdl(kern, dim3((unsigned)(tiles * a.splits)), dim3(NT), (size_t)Lt::SMEM, st, a));
   ctx->launches++;
   if (a.splits > 1) {
-    ADASK_CUDA(launch_pdl(k_gram_reduce<OUT>, dim3((unsigned)tiles, 8), dim3(256), 0, st, a));
+    // one element per thread: the split loads of every element are in flight at once
+    ADASK_CUDA(launch_pdl(k_gram_reduce<OUT>, dim3((unsigned)tiles, BT * BT / 256), dim3(256), 0, st, a));
     ctx->launches++;
   }
   return ADASK_OK;
