@@ -48,8 +48,12 @@ int fail(int status, const char* fmt, ...);
 struct Workspace {
   void* ptr = nullptr;
   size_t bytes = 0;
+  // incremented on every (re)allocation: cudaMalloc may hand back the address
+  // just freed, so a changed pointer does not detect a new (uninitialized) buffer
+  unsigned gen = 0;
   int get(size_t need, cudaStream_t st, void** out) {
     if (need > bytes) {
+      ++gen;
       if (ptr) {
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return fail(ADASK_E_CUDA, "sync: %s", cudaGetErrorString(e));
@@ -99,6 +103,7 @@ enum WsSlot {
   WS_CHOL_ITEMS, // dataflow Cholesky: helper item list (per nblk)
   WS_PAIR,       // sharded PCG proposal: the partial pair [A^T A p | A^T A x]
   WS_SA_ROWS,    // sharded build: this rank's reduce-scattered rows of SA
+  WS_SRHT_SYNC,  // fused SRHT: work ticket + per-group pass-1 counters (self-resetting)
   WS_COUNT
 };
 
@@ -137,11 +142,14 @@ struct adask_ctx {
   int device = 0;
   adask::CommState comm;
   // dataflow Cholesky (chol_df.cu): flag block identity, epoch, ticket base
-  void* chol_flags_ptr = nullptr;
+  unsigned chol_flags_gen = 0;  // Workspace::gen of the flag block last cleared
   int chol_epoch = 0;
   unsigned chol_ticket = 0;
   int chol_items_nb = -1, chol_nitems = 0;
   int64_t launches = 0;
+  // fused SRHT counters: zeroed once per allocation, reset by each launch's last CTA
+  unsigned srht_sync_gen = 0;   // Workspace::gen of the counter / map block last cleared
+  int srht_epoch = 0;
   adask::Workspace ws[adask::WS_COUNT];
   double* pinned = nullptr;  // pinned host scalars for synchronous readbacks
   int* pinned_flags = nullptr;

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -450,7 +451,9 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   ADASK_TRY(ctx->ws[WS_SIGNS].get((size_t)cdiv(1ll << ilog2(n), 32) * 4 + 64, st, &sw));  // padded: bulk-copied per tile
   ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4), 0.0, true);
   uint32_t* sgn = (uint32_t*)sw;
-  ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
+  // one fused kernel draws the signs itself; the two-launch paths draw them first
+  const bool fused = srht_fused_eligible(dtype, A, n, n_pad, lda) != 0;
+  if (!fused) ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
   // idx = choice(n_pad, m, replace=False) after the n sign draws (host)
   std::vector<int64_t> idx_own;
   if (!idx_pre || (int64_t)idx_pre->size() != m) ADASK_TRY(srht_draw_idx(g, n, m, &idx_own));
@@ -459,8 +462,9 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   const double c1 = sqrt((double)n_pad);
   const double c2 = sqrt((double)n_pad / (double)m);
   const auto h1 = std::chrono::steady_clock::now();
-  const int rc = fwht_select(ctx, dtype, A, n, d, lda, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2,
-                             (flags & ADASK_ACCUMULATE) ? 1 : 0, st);
+  const int acc = (flags & ADASK_ACCUMULATE) ? 1 : 0;
+  const int rc = fused ? srht_fused(ctx, dtype, A, n, d, lda, g, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2, acc, st)
+                       : fwht_select(ctx, dtype, A, n, d, lda, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2, acc, st);
   if (htrace) {
     const auto h2 = std::chrono::steady_clock::now();
     fprintf(stderr, "[srht host] m=%lld pre=%d signs+draw %.1f us, fwht_select %.1f us\n", (long long)m,

@@ -25,4 +25,10 @@ int fwht_tile_pass2(adask_ctx* ctx, int dtype, int L2, const void* Z, int64_t G,
                     const int32_t* d_slot_start, const int32_t* d_ent_hi, const int32_t* d_ent_k, void* out,
                     int64_t ldo, double c1, double c2, int accumulate, cudaStream_t st);
 int fwht_build_map2(adask_ctx* ctx, const int32_t* pos, int64_t m, int32_t* map2, int64_t rows, cudaStream_t st);
+// Fused SRHT (srht_fused.cu): sign draws, both passes and the selection in one
+// persistent kernel with Z L2-resident.  sgn: n_pad-bit scratch for the signs.
+int srht_fused_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int64_t lda);
+int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const adask_pcg64* g,
+               uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out, int64_t ldo, double c1,
+               double c2, int accumulate, cudaStream_t st);
 }  // namespace adask

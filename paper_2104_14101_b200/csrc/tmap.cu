@@ -1,3 +1,4 @@
+#include <cstdlib>
 // TMA tensor-map encoding (host).  cuTensorMapEncodeTiled is resolved through
 // the runtime's driver entry point, so libadask has no libcuda link dependency.
 #include <cudaTypedefs.h>
@@ -69,9 +70,15 @@ int tensor_map_rows3d(CUtensorMap* map, int dtype, const void* base, int64_t row
   cuuint64_t strides[2] = {(cuuint64_t)ld * esz * e, (cuuint64_t)ld * esz};
   cuuint32_t box[3] = {box_cols, box_q, e};
   cuuint32_t estr[3] = {1, 1, 1};
+  // L2 sector promotion of the row segments (dev probe: ADASK_TMAP_PROMO = 0 none, 1 64 B, 2 128 B, 3 256 B)
+  static const int pv = getenv("ADASK_TMAP_PROMO") ? atoi(getenv("ADASK_TMAP_PROMO")) : 3;
+  const CUtensorMapL2promotion promo = pv == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                       : pv == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                       : pv == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = encode(map, dtype == ADASK_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                       (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ADASK_E_CUDA, "cuTensorMapEncodeTiled (3-D rows) failed (%d)", (int)r);
   return ADASK_OK;
 }
