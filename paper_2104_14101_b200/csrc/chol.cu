@@ -61,7 +61,7 @@ int pad_identity(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, cuda
 }
 
 int chol_df_launch(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t kp, void* L, void* Li, void* LiT,
-                   int* info, cudaStream_t st);
+                   int* info, cudaStream_t st, int* info_mapped);
 
 static int chol_finish(adask_ctx* ctx, int* info, int64_t* info_host, cudaStream_t st) {
   if (ctx->defer_spd) {
@@ -86,9 +86,14 @@ int chol_factor_inverse(adask_ctx* ctx, int dtype, void* M, int64_t k, int64_t k
     if (kp % 32 || kp < k) return fail(ADASK_E_ARG, "chol: bad padding");
     void* wsp = nullptr;
     ADASK_TRY(ctx->ws[WS_CHOL].get(256, st, &wsp));
-    int* info = (int*)wsp;
-    ADASK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), st));
-    ADASK_TRY(chol_df_launch(ctx, dtype, M, k, kp, L, Li, LiT, info, st));
+    int* info = (int*)wsp;  // cleared by the kernel
+    if (ctx->defer_spd) {
+      // the kernel reports a failure into pinned_flags[1] itself (host-mapped)
+      ADASK_TRY(chol_df_launch(ctx, dtype, M, k, kp, L, Li, LiT, info, st, ctx->pinned_flags + 1));
+      if (info_host) *info_host = 0;
+      return ADASK_OK;
+    }
+    ADASK_TRY(chol_df_launch(ctx, dtype, M, k, kp, L, Li, LiT, info, st, nullptr));
     return chol_finish(ctx, info, info_host, st);
   }
   // tile edge: 32 unless overridden (ADASK_CHOL_NB=64)

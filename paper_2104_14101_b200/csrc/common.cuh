@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/adask.h"
@@ -145,7 +146,10 @@ struct adask_ctx {
   unsigned chol_flags_gen = 0;  // Workspace::gen of the flag block last cleared
   int chol_epoch = 0;
   unsigned chol_ticket = 0;
-  int chol_items_nb = -1, chol_nitems = 0;
+  // dataflow Cholesky helper item lists, built and uploaded once per tile
+  // count for the context's lifetime (the adaptive solves cycle through the
+  // same sizes every solve): nblk -> {device list, items}
+  std::vector<std::pair<void*, int>> chol_items;
   int64_t launches = 0;
   // fused SRHT counters: zeroed once per allocation, reset by each launch's last CTA
   unsigned srht_sync_gen = 0;   // Workspace::gen of the counter / map block last cleared

@@ -375,6 +375,8 @@ int adask_ctx_destroy(adask_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (auto& w : ctx->ws) w.release();
+  for (auto& it : ctx->chol_items)
+    if (it.first) cudaFree(it.first);
   adask::comm_release(ctx);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
