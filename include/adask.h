@@ -203,6 +203,13 @@ int adask_fwht(adask_ctx* ctx, int dtype, void* X, int64_t n, int64_t d, int64_t
 /* Problem: H X = A^T (A X) + nu^2 Lam X   (problem.py:89-107)              */
 /* ======================================================================== */
 
+/* Validation of a problem's inputs (problem.py:41-80: finite A and B, lam
+ * entries >= 1) in one pass over A: verdict[0] = 1 if A has a non-finite
+ * entry, verdict[1] = 1 if B (nb doubles) has one, verdict[2] = 1 if an entry
+ * of lam (nl doubles) is non-finite or < 1.  Synchronizes the stream.      */
+int adask_check_problem(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                        const double* B, int64_t nb, const double* lam, int64_t nl, int* verdict, void* stream);
+
 /* out[:, j] = A^T (A X[:, j]) + nu2 * lam .* X[:, j] - B[:, j]   (B nullable)
  * One pass over A per column.  With ADASK_PARTIAL only A^T A X is formed
  * (multi-GPU: all-reduce, then adask_vec_hess_finish).                     */

@@ -134,6 +134,7 @@ _PROTOS = {
     "adask_sketch_sjlt": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, i64, i64, i64, i64, P(PCG64State),
                                     P(i64), u64, vp, i64, u32, vp]),
     "adask_fwht": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, C.c_int, vp]),
+    "adask_check_problem": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, vp, i64, vp, i64, P(C.c_int), vp]),
     "adask_hess_mult": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, vp, i64, i64, dbl, vp, vp, i64, vp, i64, u32, vp]),
     "adask_hess_mult_pair": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, vp, vp, dbl, vp, vp, vp, vp]),
     "adask_vec_hess_finish": (C.c_int, [vp, vp, i64, i64, i64, vp, dbl, vp, vp, vp, vp]),

@@ -105,6 +105,7 @@ enum WsSlot {
   WS_PAIR,       // sharded PCG proposal: the partial pair [A^T A p | A^T A x]
   WS_SA_ROWS,    // sharded build: this rank's reduce-scattered rows of SA
   WS_SRHT_SYNC,  // fused SRHT: work ticket + per-group pass-1 counters (self-resetting)
+  WS_CHECK,      // problem validation verdict flags
   WS_COUNT
 };
 

@@ -21,15 +21,6 @@ from .errors import DimensionMismatch
 __all__ = ["RegularizedProblem", "ExactSolution", "direct_solve", "exact_error"]
 
 
-def _all_finite(A: torch.Tensor) -> bool:
-    """isfinite over A in row chunks (no n x d temporary for the 32-64 GB configs)."""
-    rows = max(1, (1 << 26) // max(1, A.shape[1]))
-    ok = torch.ones((), dtype=torch.bool, device=A.device)
-    for r0 in range(0, A.shape[0], rows):
-        ok &= torch.isfinite(A[r0:r0 + rows]).all()
-    return bool(ok)
-
-
 class RegularizedProblem:
     """Data matrix A (n x d), targets B (d x c), scale nu, diagonal lam
     (problem.py:41-111).  Keyword-only extras: dtype (matrix precision),
@@ -59,9 +50,15 @@ class RegularizedProblem:
             raise DimensionMismatch(f"lam must have shape ({d},), got {tuple(lam_d.shape)}")
         self.lam_dev = lam_d.contiguous()
         if validate:
-            if not bool(torch.isfinite(self.lam_dev).all()) or float(self.lam_dev.min()) < 1.0:
+            # one pass over A on the device (csrc/check.cu), one synchronization
+            verdict = (C.c_int * 3)()
+            _lib.check(_lib.lib().adask_check_problem(
+                dv.ctx().handle, dv.dtype_code(self.A_dev.dtype), self.A_dev.data_ptr(), n, d,
+                self.A_dev.stride(0) if n > 0 else d, self.Bt.data_ptr(), self.Bt.numel(), self.lam_dev.data_ptr(),
+                d, verdict, dv.stream()), "check_problem")
+            if verdict[2]:
                 raise ValueError("lam entries must be finite and >= 1")
-            if not (_all_finite(self.A_dev) and bool(torch.isfinite(self.Bt).all())):
+            if verdict[0] or verdict[1]:
                 raise ValueError("A and B must be finite")
         self.row0 = int(row0)
         self.n_total = n if n_total is None else int(n_total)
