@@ -203,7 +203,7 @@ int adask_fwht(adask_ctx* ctx, int dtype, void* X, int64_t n, int64_t d, int64_t
 /* Problem: H X = A^T (A X) + nu^2 Lam X   (problem.py:89-107)              */
 /* ======================================================================== */
 
-/* Validation of a problem's inputs (problem.py:41-80: finite A and B, lam
+/* Validation of a problem's inputs (problem.py:72-75: finite A and B, lam
  * entries >= 1) in one pass over A: verdict[0] = 1 if A has a non-finite
  * entry, verdict[1] = 1 if B (nb doubles) has one, verdict[2] = 1 if an entry
  * of lam (nl doubles) is non-finite or < 1.  Synchronizes the stream.      */

@@ -1,4 +1,4 @@
-// Problem validation in one pass      reference: problem.py:41-80 (RegularizedProblem
+// Problem validation in one pass      reference: problem.py:72-75 (RegularizedProblem
 //                                                __init__: finite A / B, lam >= 1)
 //
 // The reference checks np.isfinite(A).all(), np.isfinite(B).all() and the

@@ -1,4 +1,4 @@
-"""Problem validation (RegularizedProblem, reference problem.py:41-80) through
+"""Problem validation (RegularizedProblem, reference problem.py:72-75) through
 the one-pass device check (csrc/check.cu, adask_check_problem): non-finite A
 or B and lam entries that are non-finite or < 1 raise ValueError, as in the
 reference; valid inputs pass, for fp64 / fp32, contiguous and strided A."""
