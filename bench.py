@@ -75,7 +75,7 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
+        self._stop, self._on, self.t = threading.Event(), threading.Event(), None
         try:
             import pynvml
 
@@ -86,13 +86,11 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
-    def _sample(self, busy_only: bool):
+    def _sample(self):
         try:
             mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
-            util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
             r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-            if util > 0 or not busy_only:
-                self.samples.append(mhz)
+            self.samples.append(mhz)
             for bit, name in self.REASONS.items():
                 if r & bit and name != "gpu_idle":
                     self.reasons.add(name)
@@ -100,22 +98,31 @@ class ClockSampler:
             pass
 
     def _run(self):
+        # the thread (and NVML) are up before the timed region opens; samples
+        # are kept only while it is open (the GPU is busy throughout it)
         while not self._stop.is_set():
-            self._sample(busy_only=True)
-            time.sleep(0.002)
+            if self._on.is_set():
+                self._sample()
+            time.sleep(0.001)
 
-    def __enter__(self):
-        if self.nv:
+    def start(self):
+        if self.nv and self.t is None:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
 
+    def __enter__(self):
+        self.start()
+        self._on.set()
+        return self
+
     def __exit__(self, *a):
+        self._on.clear()
         self._stop.set()
         if self.nv:
             self.t.join()
             if not self.samples:  # a timed region shorter than the sampling period
-                self._sample(busy_only=False)
+                self._sample()
 
     def summary(self) -> dict:
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
@@ -328,6 +335,7 @@ def run_ours(args) -> None:
     def solve():
         return ak.adaptive_run(p, x0, acfg, method=cfg.method, **kw)
 
+    clk = ClockSampler(local).start()  # NVML and its thread up before the timed region
     _log("warm-up")
     for _ in range(args.warmup):
         solve()
@@ -341,7 +349,7 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    with ClockSampler(local) as clk:
+    with clk:
         ev0.record()
         evs[0].record()
         for k in range(args.steps):
