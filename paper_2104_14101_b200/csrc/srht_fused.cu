@@ -13,9 +13,8 @@
 //           reference's two steps (v / sqrt(n_pad)) * sqrt(n_pad / m).
 //
 // Prologue (every CTA, before its first item): the packed sign bits
-// integers(0, 2, size=n) (PCG64 jump-ahead, one 32-draw word per thread) and
-// the output-row map of pass 2 (epoch-tagged, so it is never cleared), then a
-// grid-wide count; the producer waits for it only before its first sign copy
+// integers(0, 2, size=n) (PCG64 jump-ahead, one 32-draw word per thread), then
+// a grid-wide count; the producer waits for it only before its first sign copy
 // (its first A tile is already in flight).  No other kernel runs per sketch.
 //
 // Schedule.  Column panels are processed in groups whose Z fits in L2; the
@@ -102,7 +101,6 @@ constexpr size_t kOffDesc = kOffSlot + kRows * 4;
 constexpr size_t kOffBar = kOffDesc + kStages * 16;
 constexpr int kXR = 4;                           // exchange-tile barriers (ring, >= kGroups)
 constexpr size_t kSmem = kOffBar + (2 * kStages + kXR) * 8;
-constexpr int kEpochBits = 11;                   // map entry = epoch << 20 | output row
 static_assert(kSmem <= 227 * 1024, "shared memory");
 
 template <typename T>
@@ -142,10 +140,9 @@ struct FusedArgs {
   uint32_t* sgn;             // packed sign bits (1 -> +1), n_pad bits (written by the prologue)
   int64_t nwords;            // n_pad / 32
   const int32_t* lo2slot;    // kRows entries, -1 = not needed
-  const int32_t* pos;        // per output row k: its Z row slot*G + hi (within a panel)
-  int64_t m;
-  int32_t* map2;             // Z row -> epoch << 20 | k (persistent, epoch-tagged)
-  int epoch;
+  const int32_t* toff;       // pass-2 tile t: its output entries are ent[toff[t] .. toff[t + 1])
+  const int32_t* ent;        // tile row << 20 | output row k, grouped by tile (host plan)
+  const uint32_t* pmask;     // per tile, per value group (kQ / R): bit e = register e is read
   unsigned char* Z;          // Z[(p * zrows + slot * G + blk) * 128 B]
   int64_t zrows;             // Z rows per panel (multiple of kRows)
   int64_t G;                 // row blocks
@@ -183,12 +180,6 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-// pass-2 map entries: written by this launch's prologue (other SMs) -> L2 only
-__device__ __forceinline__ int ld_cg(const int* p) {
-  int v;
-  asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ void discard_l2(void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
@@ -293,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_srht_fused(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap zmap, FusedArgs a) {
   using L = FL<T>;
   using V = typename L::V;
+  constexpr int kR2 = L2 > 5 ? 1 << (L2 - 5) : 1;  // pass 2: values per selected row after the register stages
   extern __shared__ __align__(128) unsigned char fsm[];
   int* s_slot = reinterpret_cast<int*>(fsm + kOffSlot);
   int4* desc = reinterpret_cast<int4*>(fsm + kOffDesc);
@@ -310,8 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   for (int i = tid; i < kRows; i += blockDim.x) s_slot[i] = a.lo2slot[i];
-  // ---- prologue: sign words (bit e of word w = draw 32 w + e; 1 -> +1) and
-  // the epoch-tagged output-row map, spread over the grid
+  // ---- prologue: sign words (bit e of word w = draw 32 w + e; 1 -> +1),
+  // spread over the grid
   for (int64_t w = blockIdx.x + (int64_t)tid * gridDim.x; w < a.nwords; w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i0 = w * 32;
     uint32_t bits = 0;
@@ -322,8 +314,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     a.sgn[w] = bits;
   }
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + tid; k < a.m; k += (int64_t)gridDim.x * blockDim.x)
-    a.map2[a.pos[k]] = (a.epoch << 20) | (int)k;
   fence_proxy_async_global();  // read next by bulk copies (async proxy)
   __syncthreads();
   if (tid == 0) {
@@ -422,14 +412,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t colb = (int64_t)panel * kRowB + c * 8;
       const int64_t nbl = a.dbytes - colb;
       const int nb = nbl >= 8 ? 8 : (nbl > 0 ? (int)nbl : 0);
-      const bool xchg = kind == 0 || L2 > 5;
 
       // round 0: rows q*32 + e, landed [e][q] (position e*kQ + q); the stage
       // is released as soon as it is in registers, so the next tile's load
       // overlaps everything below
+      // pass 2: the registers some selected row reads (0: nothing to do)
+      const uint32_t v_need = kind == 0 ? ~0u : __ldg(a.pmask + index * (kQ / kR2) + q / kR2);
       V v[32];
+      if (v_need) {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = tile[(e * kQ + q) * kLanes + c];
+        for (int e = 0; e < 32; ++e) v[e] = tile[(e * kQ + q) * kLanes + c];
+      }
       uint32_t nw = 0;
       if (kind == 0) nw = ~reinterpret_cast<const uint32_t*>(tile + kRows * kLanes)[q];
       __syncwarp();
@@ -443,34 +436,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned char* zt = a.Z + ((int64_t)panel * a.zrows + index * kRows) * kRowB;
         if (!(a.dev & 1))
           for (int l = gt; l < kTile / 128; l += kGT) discard_l2(zt + (int64_t)l * 128);
-        bfly<T, (L2 < 5 ? L2 : 5)>(v);
+        if (v_need) bfly<T, (L2 < 5 ? L2 : 5)>(v);
       }
-      // Exchange through the shared tile (row-major: one 128-byte row per
-      // half-warp both ways, conflict-free), used by the items in order: wait
-      // until item k - 1 has read it back.  Thread (c, u = q) then holds rows
-      // 32 j + u + 8 h at register 8 h + j (j = row bits 5-7, h = bits 3-4).
-      // Items use the tile in order: wait until item k - 1 has read it back.
-      // One barrier per item in a ring of kXR >= kGroups: the barrier's
-      // previous phase (item k - 1 - kXR) is complete by the time this group
-      // gets here, so the parity test is unambiguous.
+      // Exchange through the shared tile, used by the items in order: wait
+      // until item k - 1 has read it back.  One barrier per item in a ring of
+      // kXR >= kGroups: the barrier's previous phase (item k - 1 - kXR) is
+      // complete by the time this group gets here, so the parity test is
+      // unambiguous.
       if (k >= 1)
         FUSED_WAIT(mbar_test(&xdone[(k - 1) % kXR], (uint32_t)(((k - 1) / kXR) & 1)), "xdone", k);
-      if (xchg) {
+      if (kind == 0) {
+        // full exchange (row-major: one 128-byte row per half-warp both ways,
+        // conflict-free).  Thread (c, u = q) then holds rows 32 j + u + 8 h at
+        // register 8 h + j (j = row bits 5-7, h = bits 3-4).
 #pragma unroll
         for (int e = 0; e < 32; ++e) scr[(q * 32 + e) * kLanes + c] = v[e];
         named_bar_sync(1 + g, kGT);
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = scr[(32 * (i & (kQ - 1)) + q + kQ * (i >> kJB)) * kLanes + c];
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&xdone[k % kXR]);  // (every item takes one phase)
-      if (xchg) {
-        if (kind == 0)
-          bfly<T, kJB>(v);
-        else
-          bfly<T, (L2 > 5 ? L2 - 5 : 0)>(v);
-      }
-      if (kind == 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xdone[k % kXR]);  // (every item takes one phase)
+        bfly<T, kJB>(v);
         // row r of block `index` -> Z row slot(r) * G + index of the panel
         if (nb > 0) {
           unsigned char* zb = a.Z + ((int64_t)panel * a.zrows + index) * kRowB + c * 8;
@@ -486,20 +472,49 @@ __global__ void __launch_bounds__(kThreads, 1)
           __threadfence();
           atomicAdd(&a.sync[3 + it.w], 1u);
         }
-      } else if (nb > 0) {
-        // the rows' output map (epoch-tagged), eight entries per batch
-        const int* mp = a.map2 + index * kRows;
+      } else {
+        // Pass 2 finishes only the selected rows.  Tile row t = 32 q + e is
+        // Z row slot * G + blk; after the register stages (blk bits 0-4) a
+        // selected row needs the R = G / 32 values of its value group
+        // (t / 32R, e) -- threads q = (t / 32R) R + j, j = 0..R-1, register e
+        // -- combined by the remaining stages.  Only the registers some
+        // selected row reads go through the exchange tile (position
+        // ((q / R) 32 + e) R + q % R: a warp's two q are adjacent rows);
+        // thread (c, q) then finishes outputs q, q + 16, ... of the tile's
+        // list (host plan) from them, in the reference's stage order.
+        const int pb = (q / kR2) * 32 * kR2 + (q % kR2);
 #pragma unroll
-        for (int b = 0; b < 32; b += 8) {
-          int ent[8];
+        for (int e = 0; e < 32; ++e)
+          if ((v_need >> e) & 1u) scr[(pb + e * kR2) * kLanes + c] = v[e];
+        named_bar_sync(1 + g, kGT);
+        const int i1 = __ldg(a.toff + index + 1);
+        for (int i = __ldg(a.toff + index) + q; i < i1; i += kQ) {
+          const int en = __ldg(a.ent + i);
+          const int t = en >> 20;
+          const int p0 = ((t / (32 * kR2)) * 32 + (t & 31)) * kR2;
+          V w[kR2];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            ent[i] = ld_cg(mp + (xchg ? 32 * ((b + i) & (kQ - 1)) + q + kQ * ((b + i) >> kJB) : q * 32 + b + i));
+          for (int j = 0; j < kR2; ++j) w[j] = scr[(p0 + j) * kLanes + c];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if ((ent[i] >> 20) == a.epoch)
-              emit_out<T>(a, a.out + (int64_t)(ent[i] & 0xFFFFF) * a.ldo_b + colb, L::bits(v[b + i]), nb);
+          for (int h = 1; h < kR2; h <<= 1) {
+#pragma unroll
+            for (int j = 0; j < kR2; ++j) {
+              if (!(j & h)) {
+                const auto x0 = w[j], x1 = w[j + h];
+                w[j] = L::add(x0, x1);
+                w[j + h] = L::sub(x0, x1);
+              }
+            }
+          }
+          const int jh = (t >> 5) & (kR2 - 1);
+          V y = w[0];
+#pragma unroll
+          for (int j = 1; j < kR2; ++j)
+            if (jh == j) y = w[j];
+          if (nb > 0) emit_out<T>(a, a.out + (int64_t)(en & 0xFFFFF) * a.ldo_b + colb, L::bits(y), nb);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xdone[k % kXR]);
       }
     }
   }
@@ -577,7 +592,7 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
   const int W = kRowB / (int)esz;
   if (m >= (1 << 20)) return fail(ADASK_E_ARG, "srht fused: m too large");
 
-  // ---- host plan: lo -> slot, per output its Z row slot*G + hi, the segments
+  // ---- host plan: lo -> slot, the segments, per pass-2 tile its outputs
   std::vector<int32_t> lo2slot(kRows, -1);
   int64_t nslots = 0;
   for (int64_t k = 0; k < m; ++k) lo2slot[(size_t)(idx[k] & (kRows - 1))] = 0;
@@ -612,10 +627,29 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
   const int64_t n_items = t;
   if (n_items >= (1ll << 31)) return fail(ADASK_E_ARG, "srht fused: too many work items");
 
-  std::vector<int32_t> plan((size_t)(kRows + m));
+  // pass-2 tile lists: the outputs of each Z tile (tile row << 20 | k) and,
+  // per value group of kR2 threads, the registers its outputs read
+  const int R2 = L2 > 5 ? 1 << (L2 - 5) : 1;
+  const int64_t nmask = T2 * (kQ / R2);
+  const size_t o_toff = kRows, o_ent = o_toff + (size_t)T2 + 1, o_mask = o_ent + (size_t)m;
+  std::vector<int32_t> plan(o_mask + (size_t)nmask, 0);
   std::copy(lo2slot.begin(), lo2slot.end(), plan.begin());
-  for (int64_t k = 0; k < m; ++k)
-    plan[(size_t)(kRows + k)] = (int32_t)(lo2slot[(size_t)(idx[k] & (kRows - 1))] * G + (idx[k] >> kB1));
+  std::vector<int32_t> zrow((size_t)m);
+  for (int64_t k = 0; k < m; ++k) {
+    zrow[(size_t)k] = (int32_t)(lo2slot[(size_t)(idx[k] & (kRows - 1))] * G + (idx[k] >> kB1));
+    ++plan[o_toff + (size_t)(zrow[(size_t)k] / kRows) + 1];
+  }
+  for (int64_t i = 0; i < T2; ++i) plan[o_toff + (size_t)i + 1] += plan[o_toff + (size_t)i];
+  {
+    std::vector<int32_t> fill(plan.begin() + (ptrdiff_t)o_toff, plan.begin() + (ptrdiff_t)(o_toff + T2));
+    uint32_t* msk = reinterpret_cast<uint32_t*>(plan.data() + o_mask);
+    for (int64_t k = 0; k < m; ++k) {
+      const int64_t tile = zrow[(size_t)k] / kRows;
+      const int tr = (int)(zrow[(size_t)k] % kRows);
+      plan[o_ent + (size_t)fill[(size_t)tile]++] = (tr << 20) | (int32_t)k;
+      msk[tile * (kQ / R2) + tr / (32 * R2)] |= 1u << (tr & 31);
+    }
+  }
   const size_t plan_b = align_up(plan.size() * 4, 16);
   const size_t segs_b = segs.size() * sizeof(int4);
   void* pw = nullptr;
@@ -627,19 +661,15 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
 
   void* zw = nullptr;
   ADASK_TRY(ctx->ws[WS_SRHT].get((size_t)npanels * zpanel, st, &zw));
-  // counters (self-resetting) and the epoch-tagged map: zeroed once per allocation
+  // counters (self-resetting): zeroed once per allocation
   void* sw = nullptr;
   const size_t sync_b = align_up((size_t)(3 + ng) * 4 + 64, 256);
-  const size_t map_b = (size_t)zrows * 4;
-  ADASK_TRY(ctx->ws[WS_SRHT_SYNC].get(std::max<size_t>(sync_b + map_b, (size_t)1 << 20), st, &sw));
-  ctx->srht_epoch = ctx->srht_epoch + 1;
-  if (ctx->srht_sync_gen != ctx->ws[WS_SRHT_SYNC].gen || ctx->srht_epoch >= (1 << kEpochBits)) {
+  ADASK_TRY(ctx->ws[WS_SRHT_SYNC].get(std::max<size_t>(sync_b, (size_t)1 << 12), st, &sw));
+  if (ctx->srht_sync_gen != ctx->ws[WS_SRHT_SYNC].gen) {
     ADASK_CUDA(cudaMemsetAsync(sw, 0, ctx->ws[WS_SRHT_SYNC].bytes, st));
     ctx->srht_sync_gen = ctx->ws[WS_SRHT_SYNC].gen;
-    ctx->srht_epoch = 1;
   }
   unsigned* sync = (unsigned*)sw;
-  int32_t* map2 = (int32_t*)((char*)sw + sync_b);
 
   CUtensorMap am, zm;
   ADASK_TRY(tensor_map_rows3d(&am, dtype, A, n, d, lda, (uint32_t)W, kQ, 32u));
@@ -652,10 +682,9 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
   a.sgn = sgn;
   a.nwords = n_pad / 32;
   a.lo2slot = (const int32_t*)pw;
-  a.pos = (const int32_t*)pw + kRows;
-  a.m = m;
-  a.map2 = map2;
-  a.epoch = ctx->srht_epoch;
+  a.toff = (const int32_t*)pw + o_toff;
+  a.ent = (const int32_t*)pw + o_ent;
+  a.pmask = reinterpret_cast<const uint32_t*>((const int32_t*)pw + o_mask);
   a.Z = (unsigned char*)zw;
   a.zrows = zrows;
   a.G = G;
