@@ -3,9 +3,11 @@
 // S[k, i] = Philox4x32-10 / Box-Muller normal (rng.cuh) divided by sqrt(m),
 // keyed by the sketch seed and indexed by (sketch row k, GLOBAL row i of A),
 // so a row-sharded A gives per-shard partial sketches that sum to the full
-// one.  This fp64/fp32 path generates S in column chunks into HBM and runs the
-// FP64/FP32-pipe GEMM (gemm.cu); the TF32 tensor-core path with S generated
-// on the fly in shared memory is gauss_tc.cu (ADASK_TF32).
+// one.  fp64: S^T is generated in L2-sized chunks and multiplied on the FP64
+// tensor cores (DMMA, gram.cu gemm_tn_tc); fp32 without ADASK_TF32 (or
+// unaligned fp64): S chunks + the FP32/FP64-pipe GEMM (gemm.cu).  The TF32
+// tensor-core path with S generated on the fly in shared memory is
+// gauss_tc.cu (ADASK_TF32).
 #include "common.cuh"
 #include "gemm.cuh"
 #include "rng.cuh"
@@ -44,6 +46,29 @@ extern "C" int adask_sketch_gaussian_rows(adask_ctx* ctx, int dtype, const void*
   }
   if (n_local == 0) {
     if (!accumulate) ADASK_CUDA(cudaMemset2DAsync(SA, ldsa * esz, 0, d * esz, mk, st));
+    return ADASK_OK;
+  }
+  // fp64 with 16-byte aligned rows of A: FP64 tensor cores (DMMA).  S^T is
+  // generated once per chunk of rows of A (a tile-local on-the-fly generator
+  // would repeat the fp64 Box-Muller d / 128 times on the same FP64 pipe the
+  // DMMAs use).  ADASK_GAUSS_DMMA=0: the FP64-pipe GEMM;
+  // ADASK_GAUSS_CHUNK_MB: S^T bytes per chunk.
+  static const bool dmma_on = !(getenv("ADASK_GAUSS_DMMA") && atoi(getenv("ADASK_GAUSS_DMMA")) == 0);
+  static const int64_t chunk_mb = getenv("ADASK_GAUSS_CHUNK_MB") ? atoll(getenv("ADASK_GAUSS_CHUNK_MB")) : 256;
+  if (dmma_on && dtype == ADASK_F64 && ((uintptr_t)A & 15) == 0 && (lda * esz) % 16 == 0 &&
+      ((uintptr_t)SA & 7) == 0) {
+    const int64_t lds = (mk + 1) / 2 * 2;
+    int64_t nc = (int64_t)((chunk_mb << 20) / (lds * (int64_t)esz));
+    nc = std::max<int64_t>(256, nc / 256 * 256);
+    nc = std::min<int64_t>(nc, n_local);
+    void* wsp = nullptr;
+    ADASK_TRY(ctx->ws[WS_GAUSS].get((size_t)lds * nc * esz, st, &wsp));
+    for (int64_t c0 = 0; c0 < n_local; c0 += nc) {
+      const int64_t w = std::min<int64_t>(nc, n_local - c0);
+      ADASK_TRY(philox_gaussian_rows_t(ctx, dtype, k0, mk, m_total, row0 + c0, w, key, wsp, lds, st));
+      const void* Ac = (const char*)A + (size_t)c0 * lda * esz;
+      ADASK_TRY(gram::gemm_tn_tc(ctx, dtype, wsp, lds, Ac, lda, w, mk, d, SA, ldsa, c0 > 0 || accumulate, st));
+    }
     return ADASK_OK;
   }
   // chunk of S columns (rows of A) so that S_chunk stays <= 256 MiB

@@ -22,5 +22,9 @@ namespace gram {
 // plus nu2 * (lam or 1) on the diagonal, DMMA tensor cores (gram.cu).
 int gram_tc(adask_ctx* ctx, int dtype, const void* X, int64_t ld, int64_t K, int64_t N, bool kc,
             const double* rl, double nu2, const double* lam, void* M, int64_t ldm, bool out_f64, cudaStream_t st);
+// C (M x N) = X^T Y (+ C when accumulate): X K x M, Y K x N row-major with
+// 16-byte aligned rows, DMMA tensor cores with fp64 accumulation (gram.cu).
+int gemm_tn_tc(adask_ctx* ctx, int dtype, const void* X, int64_t ldx, const void* Y, int64_t ldy, int64_t K,
+               int64_t M, int64_t N, void* C, int64_t ldc, bool accumulate, cudaStream_t st);
 }  // namespace gram
 }  // namespace adask

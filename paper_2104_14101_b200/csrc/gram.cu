@@ -100,9 +100,10 @@ __device__ __forceinline__ void tile_of(int t, int& bi, int& bj) {
 // Issue the cp.async copies of one operand tile (C-index block c0) for the
 // reduction slab [k0, k0 + BK) (zero-filled past kend / N).
 template <typename T, bool KC>
-__device__ __forceinline__ void load_tile(const Args& a, uint32_t sbase, int64_t c0, int64_t k0, int64_t kend) {
+__device__ __forceinline__ void load_tile(const void* Xv, int64_t ld, int64_t N, uint32_t sbase, int64_t c0,
+                                          int64_t k0, int64_t kend) {
   using Lt = Lay<T, KC>;
-  const T* X = reinterpret_cast<const T*>(a.X);
+  const T* X = reinterpret_cast<const T*>(Xv);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int c = threadIdx.x + NT * q;  // chunk 0..1023
@@ -114,7 +115,7 @@ __device__ __forceinline__ void load_tile(const Args& a, uint32_t sbase, int64_t
       cc = (c % (BT / Lt::V)) * Lt::V;
       grow = k0 + r;
       gcol = c0 + cc;
-      const int64_t left = a.N - gcol;
+      const int64_t left = N - gcol;
       bytes = (grow < kend && left > 0) ? (int)(left >= Lt::V ? 16 : left * Lt::ES) : 0;
     } else {
       r = c / (Lt::BK / Lt::V);
@@ -122,9 +123,9 @@ __device__ __forceinline__ void load_tile(const Args& a, uint32_t sbase, int64_t
       grow = c0 + r;
       gcol = k0 + cc;
       const int64_t left = kend - gcol;
-      bytes = (grow < a.N && left > 0) ? (int)(left >= Lt::V ? 16 : left * Lt::ES) : 0;
+      bytes = (grow < N && left > 0) ? (int)(left >= Lt::V ? 16 : left * Lt::ES) : 0;
     }
-    const T* g = bytes ? X + grow * a.ld + gcol : X;
+    const T* g = bytes ? X + grow * ld + gcol : X;
     cp_async16(sbase + (uint32_t)(r * Lt::PITCH_B + cc * Lt::ES), g, bytes);
   }
 }
@@ -162,8 +163,8 @@ __global__ void __launch_bounds__(NT, 1) k_gram_dmma(Args a) {
   auto issue = [&](int stage_slot, int st_idx) {
     const uint32_t sb = s0 + (uint32_t)(stage_slot * Lt::STAGE_BYTES);
     const int64_t k0 = kbeg + (int64_t)st_idx * Lt::BK;
-    load_tile<T, KC>(a, sb, ci, k0, kend);
-    if (!diag) load_tile<T, KC>(a, sb + Lt::OP_BYTES, cj, k0, kend);
+    load_tile<T, KC>(a.X, a.ld, a.N, sb, ci, k0, kend);
+    if (!diag) load_tile<T, KC>(a.X, a.ld, a.N, sb + Lt::OP_BYTES, cj, k0, kend);
   };
 
 #pragma unroll
@@ -342,6 +343,185 @@ int run(adask_ctx* ctx, Args a, cudaStream_t st) {
   if (a.splits > 1) {
     // one element per thread: the split loads of every element are in flight at once
     ADASK_CUDA(launch_pdl(k_gram_reduce<OUT>, dim3((unsigned)tiles, BT * BT / 256), dim3(256), 0, st, a));
+    ctx->launches++;
+  }
+  return ADASK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Rectangular C (M x N) = X^T Y (+ C), X K x M and Y K x N row-major: the same
+// K-outer DMMA tile kernel over a full tile grid.  Used by the fp64 Gaussian
+// sketch (gauss.cu): X = S^T chunk (Philox normals, generated once per chunk
+// and L2-resident), Y = the rows of A of the chunk.  Deterministic split-K.
+struct RArgs {
+  const void* X;
+  int64_t ldx;
+  const void* Y;
+  int64_t ldy;
+  int64_t K, M, N;
+  int nbn;           // C tiles per row of tiles
+  int splits;
+  int64_t kchunk;
+  void* C;
+  int64_t ldc;
+  int accumulate;
+  double* part;      // splits > 1: [tile][split][BT][BT]
+};
+
+template <typename T, typename OUT>
+__global__ void __launch_bounds__(NT, 1) k_gemm_tn_dmma(RArgs a) {
+  using Lt = Lay<T, false>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  pdl_wait();
+  const int tile = blockIdx.x / a.splits, split = blockIdx.x % a.splits;
+  const int bi = tile / a.nbn, bj = tile % a.nbn;
+  const int64_t ci = (int64_t)bi * BT, cj = (int64_t)bj * BT;
+  const int64_t kbeg = (int64_t)split * a.kchunk;
+  const int64_t kend = min(a.K, kbeg + a.kchunk);
+  const int nst = kend > kbeg ? (int)((kend - kbeg + Lt::BK - 1) / Lt::BK) : 0;
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  const bool active = (ci + wm * 64 < a.M) && (cj + wn * 32 < a.N);
+
+  double acc[4][4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+  auto issue = [&](int stage_slot, int st_idx) {
+    const uint32_t sb = s0 + (uint32_t)(stage_slot * Lt::STAGE_BYTES);
+    const int64_t k0 = kbeg + (int64_t)st_idx * Lt::BK;
+    load_tile<T, false>(a.X, a.ldx, a.M, sb, ci, k0, kend);
+    load_tile<T, false>(a.Y, a.ldy, a.N, sb + Lt::OP_BYTES, cj, k0, kend);
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nst) issue(s, s);
+    cp_commit();
+  }
+  for (int it = 0; it < nst; ++it) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nx = it + STAGES - 1;
+      if (nx < nst) issue(nx % STAGES, nx);
+      cp_commit();
+    }
+    if (!active) continue;
+    const unsigned char* sb = smem + (it % STAGES) * Lt::STAGE_BYTES;
+    const T* As = reinterpret_cast<const T*>(sb);
+    const T* Bs = reinterpret_cast<const T*>(sb + Lt::OP_BYTES);
+#pragma unroll
+    for (int q = 0; q < Lt::BK / 4; ++q) {  // fragment <-> C index permutation as in k_gram_dmma
+      const T* arow = As + (4 * q + tig) * Lt::PITCH + wm * 64 + 2 * g;
+      const T* brow = Bs + (4 * q + tig) * Lt::PITCH + wn * 32 + 2 * g;
+      double2 av[4], bv[2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) av[mi] = lds2<T>(arow + 16 * mi);
+#pragma unroll
+      for (int np = 0; np < 2; ++np) bv[np] = lds2<T>(brow + 16 * np);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        dmma(acc[mi][0], av[mi].x, av[mi].y, bv[0].x);
+        dmma(acc[mi][1], av[mi].x, av[mi].y, bv[0].y);
+        dmma(acc[mi][2], av[mi].x, av[mi].y, bv[1].x);
+        dmma(acc[mi][3], av[mi].x, av[mi].y, bv[1].y);
+      }
+    }
+  }
+  cp_wait<0>();
+  if (!active && a.splits == 1) return;
+  const bool direct = a.splits == 1;
+  double* part = direct ? nullptr : a.part + ((int64_t)tile * a.splits + split) * (BT * BT);
+  OUT* C = reinterpret_cast<OUT*>(a.C);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = wm * 64 + 16 * mi + 2 * g + (e >> 1);
+        const int c = wn * 32 + 16 * (ni >> 1) + 2 * (2 * tig + (e & 1)) + (ni & 1);
+        const double v = acc[mi][ni][e];
+        if (!direct) {
+          part[r * BT + c] = v;
+        } else {
+          const int64_t gr = ci + r, gc = cj + c;
+          if (gr < a.M && gc < a.N) {
+            OUT* o = C + gr * a.ldc + gc;
+            *o = (OUT)(a.accumulate ? (double)*o + v : v);
+          }
+        }
+      }
+}
+
+template <typename OUT>
+__global__ void k_gemm_tn_reduce(RArgs a) {
+  pdl_wait();
+  const int tile = blockIdx.x;
+  const int bi = tile / a.nbn, bj = tile % a.nbn;
+  const int64_t ci = (int64_t)bi * BT, cj = (int64_t)bj * BT;
+  const double* P = a.part + (int64_t)tile * a.splits * (BT * BT);
+  OUT* C = reinterpret_cast<OUT*>(a.C);
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < BT * BT; e += gridDim.y * blockDim.x) {
+    const int r = e / BT, c = e % BT;
+    const int64_t gr = ci + r, gc = cj + c;
+    if (gr >= a.M || gc >= a.N) continue;
+    double v = 0.0;
+    for (int s = 0; s < a.splits; ++s) v += P[(int64_t)s * (BT * BT) + e];
+    OUT* o = C + gr * a.ldc + gc;
+    *o = (OUT)(a.accumulate ? (double)*o + v : v);
+  }
+}
+
+// C (M x N, dtype) = X^T Y (+ C): X K x M, Y K x N, both `dtype`, 16-byte
+// aligned rows (the caller checks).
+int gemm_tn_tc(adask_ctx* ctx, int dtype, const void* X, int64_t ldx, const void* Y, int64_t ldy, int64_t K,
+               int64_t M, int64_t N, void* C, int64_t ldc, bool accumulate, cudaStream_t st) {
+  if (M < 1 || N < 1) return ADASK_OK;
+  RArgs a{};
+  a.X = X;
+  a.ldx = ldx;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.K = K;
+  a.M = M;
+  a.N = N;
+  a.C = C;
+  a.ldc = ldc;
+  a.accumulate = accumulate ? 1 : 0;
+  a.nbn = (int)cdiv(N, BT);
+  const int tiles = (int)cdiv(M, BT) * a.nbn;
+  const int BK = dtype == ADASK_F64 ? Lay<double, false>::BK : Lay<float, false>::BK;
+  const int64_t ksteps = std::max<int64_t>(1, cdiv(K, BK));
+  a.splits = choose_splits(tiles, ksteps);
+  a.kchunk = cdiv(ksteps, a.splits) * BK;
+  a.splits = (int)std::max<int64_t>(1, cdiv(K, a.kchunk));
+  if (a.splits > 1) {
+    void* w = nullptr;
+    ADASK_TRY(ctx->ws[WS_GEMM].get((size_t)tiles * a.splits * BT * BT * sizeof(double), st, &w));
+    a.part = (double*)w;
+  }
+  if (dtype == ADASK_F64) {
+    auto kern = k_gemm_tn_dmma<double, double>;
+    ADASK_TRY(ensure_smem_attr((const void*)kern, Lay<double, false>::SMEM));
+    ADASK_CUDA(launch_pdl(kern, dim3((unsigned)(tiles * a.splits)), dim3(NT), (size_t)Lay<double, false>::SMEM, st, a));
+  } else {
+    auto kern = k_gemm_tn_dmma<float, float>;
+    ADASK_TRY(ensure_smem_attr((const void*)kern, Lay<float, false>::SMEM));
+    ADASK_CUDA(launch_pdl(kern, dim3((unsigned)(tiles * a.splits)), dim3(NT), (size_t)Lay<float, false>::SMEM, st, a));
+  }
+  ctx->launches++;
+  if (a.splits > 1) {
+    if (dtype == ADASK_F64)
+      ADASK_CUDA(launch_pdl(k_gemm_tn_reduce<double>, dim3((unsigned)tiles, BT * BT / 256), dim3(256), 0, st, a));
+    else
+      ADASK_CUDA(launch_pdl(k_gemm_tn_reduce<float>, dim3((unsigned)tiles, BT * BT / 256), dim3(256), 0, st, a));
     ctx->launches++;
   }
   return ADASK_OK;

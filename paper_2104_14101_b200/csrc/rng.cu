@@ -214,6 +214,40 @@ int philox_gaussian_rows(adask_ctx* ctx, int dtype, int64_t krow0, int64_t mk, i
   return ADASK_OK;
 }
 
+// The same entries stored transposed: out[(i - col0) * ldo + (k - krow0)] =
+// S[k, i] (rows = columns of S = rows of A), the K-outer operand of the DMMA
+// sketch GEMM.  Consecutive threads take consecutive row groups of one column.
+template <typename T>
+__global__ void k_philox_gaussian_t(int64_t krow0, int64_t mk, int64_t col0, int64_t ncols, int64_t groups,
+                                    uint32_t k0, uint32_t k1, double sc, T* __restrict__ out, int64_t ldo) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ncols * groups) return;
+  const int64_t c = t / groups;
+  const int64_t g = (krow0 >> 2) + (t - c * groups);
+  double z[4];
+  gaussian_quad_f64((uint64_t)(col0 + c), (uint32_t)g, k0, k1, z);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t k = 4 * g + q;
+    if (k >= krow0 && k < krow0 + mk) out[c * ldo + (k - krow0)] = (T)(z[q] / sc);
+  }
+}
+
+int philox_gaussian_rows_t(adask_ctx* ctx, int dtype, int64_t krow0, int64_t mk, int64_t m_total, int64_t col0,
+                           int64_t ncols, uint64_t key, void* out, int64_t ldo, cudaStream_t st) {
+  if (mk <= 0 || ncols <= 0) return ADASK_OK;
+  const int64_t groups = ((krow0 + mk - 1) >> 2) - (krow0 >> 2) + 1;
+  const double sc = sqrt((double)m_total);
+  const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+  const unsigned grid = (unsigned)cdiv(ncols * groups, 256);
+  if (dtype == ADASK_F64)
+    k_philox_gaussian_t<double><<<grid, 256, 0, st>>>(krow0, mk, col0, ncols, groups, k0, k1, sc, (double*)out, ldo);
+  else
+    k_philox_gaussian_t<float><<<grid, 256, 0, st>>>(krow0, mk, col0, ncols, groups, k0, k1, sc, (float*)out, ldo);
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
+}
+
 }  // namespace adask
 
 using namespace adask;

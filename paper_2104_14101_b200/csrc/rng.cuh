@@ -103,6 +103,10 @@ __host__ __device__ inline void gaussian_quad_f64(uint64_t i, uint32_t g, uint32
 int philox_gaussian_rows(adask_ctx* ctx, int dtype, int64_t krow0, int64_t mk, int64_t m_total, int64_t col0,
                          int64_t ncols, uint64_t key, void* out, int64_t ldo, cudaStream_t st);
 
+// The same rows stored transposed (out[(i - col0) * ldo + (k - krow0)] = S[k, i], ldo >= mk).
+int philox_gaussian_rows_t(adask_ctx* ctx, int dtype, int64_t krow0, int64_t mk, int64_t m_total, int64_t col0,
+                           int64_t ncols, uint64_t key, void* out, int64_t ldo, cudaStream_t st);
+
 // Items [item0, item0 + count) of Generator.integers(0, m, size=total_items)
 // whose draws start at index `first`; *next = draw index after the last item
 // of the whole call (total_items).

@@ -102,3 +102,57 @@ def test_gram_no_library_kernels(ak):
 
     out = subprocess.run(["ldd", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "cublas" not in out.lower()
+
+
+# ---- fp64 Gaussian sketch on the FP64 tensor cores (gauss.cu -> gemm_tn_tc):
+# S^T chunks (Philox, transposed) times the rows of A, embeddings.py:66-73
+@pytest.mark.parametrize("n,d,m", [(1, 2, 1), (37, 6, 5), (2000, 96, 50), (4096, 256, 16), (4096, 256, 300),
+                                   (20000, 130, 129), (65536, 384, 260)])
+def test_gaussian_fp64_dmma_matches_injected_oracle(ak, n, d, m):
+    from oracle import adasketch_oracle as O
+    from paper_2104_14101_b200.embeddings import gaussian_dev
+
+    rng = np.random.default_rng(n + 3 * d + m)
+    A = rng.standard_normal((n, d))
+    got = gaussian_dev(torch.from_numpy(A).cuda(), m, 77, row0=5).cpu().numpy()
+    S = O.philox_gaussian(m, n, 77, col0=5)
+    ref = S @ A
+    assert _rel(got, ref) <= 1e-13
+    # elementwise: fp64 accumulation error only
+    assert np.all(np.abs(got - ref) <= 1e-13 * (np.abs(S) @ np.abs(A)) + 1e-300)
+
+
+def test_gaussian_fp64_dmma_shards_and_pipe_variant(ak, monkeypatch):
+    """Row shards accumulate to the whole sketch, and the FP64-pipe GEMM
+    (unaligned rows of A take it) agrees with the DMMA path."""
+    from paper_2104_14101_b200.embeddings import gaussian_dev
+
+    rng = np.random.default_rng(9)
+    A = torch.from_numpy(rng.standard_normal((6000, 200))).cuda()
+    whole = gaussian_dev(A, 72, 3)
+    part = gaussian_dev(A[:2500].contiguous(), 72, 3)
+    part = gaussian_dev(A[2500:].contiguous(), 72, 3, row0=2500, out=part, accumulate=True)
+    torch.testing.assert_close(part, whole, rtol=0, atol=1e-12)
+    # odd leading dimension: rows not 16-byte aligned -> FP64-pipe path
+    Ao = torch.empty((6000, 201), dtype=torch.float64, device="cuda")[:, :200]
+    Ao.copy_(A)
+    assert Ao.stride(0) == 201
+    pipe = gaussian_dev(Ao, 72, 3)
+    torch.testing.assert_close(pipe, whole, rtol=0, atol=1e-12)
+
+
+def test_gaussian_fp64_uses_dmma_kernel(ak):
+    """The fp64 Gaussian launches the repo's DMMA GEMM (profiler kernel names)."""
+    from torch.profiler import ProfilerActivity, profile
+
+    from paper_2104_14101_b200.embeddings import gaussian_dev
+
+    A = torch.randn((8192, 256), dtype=torch.float64, device="cuda")
+    gaussian_dev(A, 64, 1)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        gaussian_dev(A, 64, 1)
+        torch.cuda.synchronize()
+    names = [e.key for e in prof.key_averages()]
+    assert any("k_gemm_tn_dmma" in k for k in names), names
+    assert not any(("cutlass" in k or "cublas" in k.lower() or "gemm_kernel" in k) for k in names), names
