@@ -41,8 +41,8 @@
 //     half-warp both ways: conflict-free), bits 5-8 (pass 2: 5..L2-1) on the
 //     transposed registers, stores straight from registers.
 //
-// Measured on the B200 (tools/srht_fused_bench.py, 2^16 x 1024 fp64): 138 us
-// (m = 32) .. 297 us (m = 4096) per sketch against 164 .. 354 us for the
+// Measured on the B200 (tools/srht_fused_bench.py, 2^16 x 1024 fp64): 135 us
+// (m = 32) .. 271 us (m = 4096) per sketch against 164 .. 354 us for the
 // two-launch TMA pipeline of srht_pipe.cu.  What bounds it: the loads in
 // flight.  A 64 KB tile per stage and the 64 KB exchange tile leave room for
 // two stages per SM; the load-only probe (consumers releasing at once, three
@@ -51,7 +51,12 @@
 // three stages with the exchange in place (139 us, stages held through the
 // exchange), 256-row tiles with six stages (the shared exchange tile
 // serializes twice as many items: 182 us), L2 prefetch of the next four
-// tiles (no gain).
+// tiles (no gain), a half-width exchange tile (eight lanes per round, two
+// rounds) making room for a third stage shared round-robin (271 us at m = 32:
+// 8-byte shared accesses are issued per half-warp, so a half-active round
+// costs as many wavefronts as a full one), a per-thread mask of the
+// registers that have a Z slot in front of the slot lookups (168 us: the
+// extra live register tips the 96-register consumer loop into worse code).
 //
 // Algorithmic bytes per sketch: (n + m) * d * sizeof(T).
 #include <algorithm>
