@@ -60,6 +60,7 @@
 //
 // Algorithmic bytes per sketch: (n + m) * d * sizeof(T).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -105,7 +106,10 @@ constexpr size_t kOffSlot = kOffScr + kTile;
 constexpr size_t kOffDesc = kOffSlot + kRows * 4;
 constexpr size_t kOffBar = kOffDesc + kStages * 16;
 constexpr int kXR = 4;                           // exchange-tile barriers (ring, >= kGroups)
-constexpr size_t kSmem = kOffBar + (2 * kStages + kXR) * 8;
+// publisher mailboxes (kRegSplit): per group {seq, done, ring[kPubRing]}
+constexpr int kPubRing = 8;
+constexpr size_t kOffPub = kOffBar + (2 * kStages + kXR) * 8;
+constexpr size_t kSmem = kOffPub + kGroups * (2 + kPubRing) * 4;
 static_assert(kSmem <= 227 * 1024, "shared memory");
 
 template <typename T>
@@ -162,7 +166,25 @@ struct FusedArgs {
   const int4* segs;          // {kind, group, first ticket, count}
   unsigned* sync;            // [0] ticket, [1] exit count, [2] prologue count, [3 + g] pass-1 items of group g
   int dev;                   // dev switches: bit 0 no L2 discard of Z, bit 1 default L2 policy for Z
+  unsigned long long* tlog;  // -DFUSED_TRACE: per CTA and group, per item {kind, t_wait, t_full, t_xwait, t_x, t_done}
 };
+#ifdef FUSED_TRACE
+constexpr int kTraceItems = 96;  // per (CTA, group)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define FTRACE(slot)                                                                                     \
+  do {                                                                                                   \
+    if (a.tlog && gt == 0 && n < kTraceItems)                                                            \
+      a.tlog[(((size_t)blockIdx.x * kGroups + g) * kTraceItems + n) * 12 + (slot)] = gtimer();            \
+  } while (0)
+#else
+#define FTRACE(slot) \
+  do {               \
+  } while (0)
+#endif
 
 __device__ __forceinline__ uint64_t pol_evict_last() {
   uint64_t p;
@@ -291,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using V = typename L::V;
   constexpr int kR2 = L2 > 5 ? 1 << (L2 - 5) : 1;  // pass 2: values per selected row after the register stages
   extern __shared__ __align__(128) unsigned char fsm[];
-  int* s_slot = reinterpret_cast<int*>(fsm + kOffSlot);
+  unsigned short* s_slot = reinterpret_cast<unsigned short*>(fsm + kOffSlot);
   int4* desc = reinterpret_cast<int4*>(fsm + kOffDesc);
   uint64_t* full = reinterpret_cast<uint64_t*>(fsm + kOffBar);
   uint64_t* empty = full + kStages;
@@ -305,8 +327,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < kXR; ++i) mbar_init(&xdone[i], kGT / 32);
     fence_barrier_init();
+    for (int i = 0; i < kGroups * (2 + kPubRing); ++i) reinterpret_cast<int*>(fsm + kOffPub)[i] = 0;
   }
-  for (int i = tid; i < kRows; i += blockDim.x) s_slot[i] = a.lo2slot[i];
+  // slot of row 32 j + key (key = q + kQ hh: the rows of one thread after the
+  // exchange, register j + kQ hh) at [key][j], 16 bits each (0xFFFF: no slot):
+  // a thread fetches its 32 slots with 16-byte loads
+  static_assert(kQ % 8 == 0 && kRows <= 0xFFFF, "slot table");
+  for (int i = tid; i < kRows; i += blockDim.x) {
+    const int row = 32 * (i % kQ) + i / kQ;
+    s_slot[i] = (unsigned short)a.lo2slot[row];
+  }
   // ---- prologue: sign words (bit e of word w = draw 32 w + e; 1 -> +1),
   // spread over the grid
   for (int64_t w = blockIdx.x + (int64_t)tid * gridDim.x; w < a.nwords; w += (int64_t)gridDim.x * blockDim.x) {
@@ -328,6 +358,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= kGroups * kGT / 32) {  // --------------------------- producer
     if constexpr (kRegSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProducer));
+    if (kRegSplit && warp > kGroups * kGT / 32 && warp <= kGroups * kGT / 32 + kGroups && lane == 0) {
+      // publisher of consumer group pg: the release fence + count of a
+      // finished pass-1 item costs ~1 us (measured), so it runs here, off the
+      // consumers' path.  The group's thread 0 posts the column group after
+      // the barrier that follows the item's Z stores (release.cta); this
+      // thread's acquire + gpu-scope fence make them visible before the count.
+      const int pg = warp - kGroups * kGT / 32 - 1;
+      volatile int* mb = reinterpret_cast<volatile int*>(fsm + kOffPub) + pg * (2 + kPubRing);
+      int done = 0;
+      for (;;) {
+        int seq;
+        asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(seq) : "r"(smem_u32((const void*)mb)) : "memory");
+        if (seq == done) {
+          __nanosleep(40);
+          continue;
+        }
+        const int grp = mb[2 + done % kPubRing];
+        ++done;
+        mb[1] = done;
+        if (grp < 0) break;
+        __threadfence();
+        atomicAdd(&a.sync[3 + grp], 1u);
+      }
+    }
     if (warp == kGroups * kGT / 32 && lane == 0) {
       umma::tma_prefetch_map(&amap);
       umma::tma_prefetch_map(&zmap);
@@ -404,13 +458,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int gt = tid - g * kGT, c = gt & (kLanes - 1), q = gt >> 4;
     const uint64_t pol_zw = (a.dev & 2) ? policy_evict_normal() : pol_evict_last();
     V* scr = reinterpret_cast<V*>(fsm + kOffScr);
+    volatile int* mb = reinterpret_cast<volatile int*>(fsm + kOffPub) + g * (2 + kPubRing);
+    int nposted = 0;
+    // thread 0 of the group, after the barrier that follows the item's Z
+    // stores: hand the count to the publisher warp (grp < 0: exit)
+    auto post = [&](int grp) {
+      if (gt != 0) return;
+      if constexpr (kRegSplit) {
+        while (nposted - mb[1] >= kPubRing) {
+        }
+        mb[2 + nposted % kPubRing] = grp;
+        ++nposted;
+        asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32((const void*)mb)), "r"(nposted) : "memory");
+      } else if (grp >= 0) {
+        __threadfence();
+        atomicAdd(&a.sync[3 + grp], 1u);
+      }
+    };
 #pragma unroll 1
     for (int n = 0;; ++n) {
       const int k = n * kGroups + g;
       const int s = g * kRing + n % kRing;
+      FTRACE(1);
       FUSED_WAIT(mbar_test(&full[s], (uint32_t)((n / kRing) & 1)), "full", k);
       const int4 it = desc[s];
-      if (it.x < 0) break;
+      if (it.x < 0) {
+        post(-1);
+        break;
+      }
+      FTRACE(2);
+#ifdef FUSED_TRACE
+      if (a.tlog && gt == 0 && n < kTraceItems)
+        a.tlog[(((size_t)blockIdx.x * kGroups + g) * kTraceItems + n) * 12] = 1 + it.x;
+#endif
       const V* tile = reinterpret_cast<const V*>(fsm + (size_t)s * kStage);
       const int kind = it.x, panel = it.y;
       const int64_t index = it.z;
@@ -448,8 +528,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // kXR >= kGroups: the barrier's previous phase (item k - 1 - kXR) is
       // complete by the time this group gets here, so the parity test is
       // unambiguous.
+      FTRACE(3);
       if (k >= 1)
         FUSED_WAIT(mbar_test(&xdone[(k - 1) % kXR], (uint32_t)(((k - 1) / kXR) & 1)), "xdone", k);
+      FTRACE(4);
       if (kind == 0) {
         // full exchange (row-major: one 128-byte row per half-warp both ways,
         // conflict-free).  Thread (c, u = q) then holds rows 32 j + u + 8 h at
@@ -461,22 +543,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 32; ++i) v[i] = scr[(32 * (i & (kQ - 1)) + q + kQ * (i >> kJB)) * kLanes + c];
         __syncwarp();
         if (lane == 0) mbar_arrive(&xdone[k % kXR]);  // (every item takes one phase)
+        FTRACE(5);
         bfly<T, kJB>(v);
+        FTRACE(10);
         // row r of block `index` -> Z row slot(r) * G + index of the panel
         if (nb > 0) {
           unsigned char* zb = a.Z + ((int64_t)panel * a.zrows + index) * kRowB + c * 8;
+          const uint32_t gstride = (uint32_t)a.G * kRowB;  // slot * gstride < 2^32 (L <= 18)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int sl = s_slot[32 * (i & (kQ - 1)) + q + kQ * (i >> kJB)];
-            if (sl >= 0) st_z(zb + (int64_t)sl * a.G * kRowB, L::bits(v[i]), pol_zw);
+          for (int hh = 0; hh < 32 / kQ; ++hh) {
+            const uint4* sp = reinterpret_cast<const uint4*>(s_slot + (q + kQ * hh) * kQ);
+#pragma unroll
+            for (int j8 = 0; j8 < kQ / 8; ++j8) {
+              const uint4 sv = sp[j8];
+              const uint32_t w4[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                const uint32_t sl = (w4[jj >> 1] >> (16 * (jj & 1))) & 0xFFFFu;
+                if (sl != 0xFFFFu)
+                  st_z(zb + (uint64_t)sl * gstride, L::bits(v[kQ * hh + 8 * j8 + jj]), pol_zw);
+              }
+            }
           }
         }
+        FTRACE(7);
         fence_proxy_async_global();  // Z is read next by TMA
+        FTRACE(8);
         named_bar_sync(1 + g, kGT);  // every Z store of the item issued
-        if (gt == 0) {
-          __threadfence();
-          atomicAdd(&a.sync[3 + it.w], 1u);
-        }
+        FTRACE(9);
+        post(it.w);
+        FTRACE(6);
       } else {
         // Pass 2 finishes only the selected rows.  Tile row t = 32 q + e is
         // Z row slot * G + blk; after the register stages (blk bits 0-4) a
@@ -520,6 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&xdone[k % kXR]);
+        FTRACE(6);
       }
     }
   }
@@ -705,8 +802,29 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
   a.segs = (const int4*)((const char*)pw + plan_b);
   a.sync = sync;
   a.dev = getenv("ADASK_SRHT_FUSED_DEV") ? atoi(getenv("ADASK_SRHT_FUSED_DEV")) : 0;
+#ifdef FUSED_TRACE
+  // development build: per-item timestamps dumped to the file named by ADASK_SRHT_FUSED_TRACE
+  const char* tr = getenv("ADASK_SRHT_FUSED_TRACE");
+  const size_t tl_n = (size_t)kNumSMs * kGroups * kTraceItems * 12;
+  if (tr) {
+    ADASK_CUDA(cudaMalloc(&a.tlog, tl_n * 8));
+    ADASK_CUDA(cudaMemsetAsync(a.tlog, 0, tl_n * 8, st));
+  }
+#endif
   const int rc = dtype == ADASK_F64 ? launch_fused<double>(ctx, L2, am, zm, a, st)
                                     : launch_fused<float>(ctx, L2, am, zm, a, st);
+#ifdef FUSED_TRACE
+  if (tr && rc == ADASK_OK) {
+    std::vector<unsigned long long> h(tl_n);
+    ADASK_CUDA(cudaStreamSynchronize(st));
+    ADASK_CUDA(cudaMemcpy(h.data(), a.tlog, tl_n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(a.tlog);
+    if (FILE* f = fopen(tr, "wb")) {
+      fwrite(h.data(), 8, tl_n, f);
+      fclose(f);
+    }
+  }
+#endif
   return rc;
 }
 
