@@ -56,7 +56,10 @@
 // 8-byte shared accesses are issued per half-warp, so a half-active round
 // costs as many wavefronts as a full one), a per-thread mask of the
 // registers that have a Z slot in front of the slot lookups (168 us: the
-// extra live register tips the 96-register consumer loop into worse code).
+// extra live register tips the 96-register consumer loop into worse code),
+// pass-2 tile records (entry count, masks, entries) copied into shared
+// memory next to the Z tile by the producer instead of read-only global
+// loads in the consumers (no gain: those loads hit L1 / L2 off the path).
 //
 // Algorithmic bytes per sketch: (n + m) * d * sizeof(T).
 #include <algorithm>
