@@ -106,6 +106,8 @@ enum WsSlot {
   WS_SA_ROWS,    // sharded build: this rank's reduce-scattered rows of SA
   WS_SRHT_SYNC,  // fused SRHT: work ticket + per-group pass-1 counters (self-resetting)
   WS_CHECK,      // problem validation verdict flags
+  WS_SRHT_PART,  // big-block SRHT: per-sub-block partial rows
+  WS_SRHT_MAP,   // big-block SRHT: selected row -> partial row, high bits
   WS_COUNT
 };
 

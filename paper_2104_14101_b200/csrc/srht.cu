@@ -452,7 +452,8 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   ProfScope prof(ctx, PK_SRHT, st, (double)(n + m) * d * (dtype == ADASK_F64 ? 8 : 4), 0.0, true);
   uint32_t* sgn = (uint32_t*)sw;
   // one fused kernel draws the signs itself; the two-launch paths draw them first
-  const bool fused = srht_fused_eligible(dtype, A, n, n_pad, lda) != 0;
+  const bool big = srht_fused_big_eligible(dtype, A, n, n_pad, lda, m) != 0;
+  const bool fused = big || srht_fused_eligible(dtype, A, n, n_pad, lda) != 0;
   if (!fused) ADASK_TRY(pcg_sign_bits_impl(ctx, g, 0, n, sgn, st));
   // idx = choice(n_pad, m, replace=False) after the n sign draws (host)
   std::vector<int64_t> idx_own;
@@ -463,7 +464,8 @@ int sketch_srht_impl(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_
   const double c2 = sqrt((double)n_pad / (double)m);
   const auto h1 = std::chrono::steady_clock::now();
   const int acc = (flags & ADASK_ACCUMULATE) ? 1 : 0;
-  const int rc = fused ? srht_fused(ctx, dtype, A, n, d, lda, g, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2, acc, st)
+  const int rc = big ? srht_fused_big(ctx, dtype, A, n, d, lda, g, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2, acc, st)
+               : fused ? srht_fused(ctx, dtype, A, n, d, lda, g, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2, acc, st)
                        : fwht_select(ctx, dtype, A, n, d, lda, sgn, n_pad, idx.data(), m, SA, ldsa, c1, c2, acc, st);
   if (htrace) {
     const auto h2 = std::chrono::steady_clock::now();

@@ -31,4 +31,9 @@ int srht_fused_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int6
 int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const adask_pcg64* g,
                uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out, int64_t ldo, double c1,
                double c2, int accumulate, cudaStream_t st);
+// 2^19 .. 2^22 padded rows: the fused kernel per 2^18-row sub-block + a combine of the partials.
+int srht_fused_big_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int64_t lda, int64_t m);
+int srht_fused_big(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                   const adask_pcg64* g, uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out,
+                   int64_t ldo, double c1, double c2, int accumulate, cudaStream_t st);
 }  // namespace adask

@@ -148,7 +148,8 @@ struct FL<float> {
 struct FusedArgs {
   int64_t n_valid;           // rows of A (= sign draws)
   int64_t dbytes;            // d * sizeof(T)
-  GenState gen;              // generator at the first sign draw
+  GenState gen;              // generator at the first sign draw of the whole transform
+  uint64_t draw0;            // first sign draw of this (sub-)block
   uint32_t* sgn;             // packed sign bits (1 -> +1), n_pad bits (written by the prologue)
   int64_t nwords;            // n_pad / 32
   const int32_t* lo2slot;    // kRows entries, -1 = not needed
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t bits = 0;
     if (i0 < a.n_valid) {
       const int cnt = a.n_valid - i0 < 32 ? (int)(a.n_valid - i0) : 32;
-      U32Stream st(a.gen, (uint64_t)i0);
+      U32Stream st(a.gen, a.draw0 + (uint64_t)i0);
       for (int e = 0; e < cnt; ++e) bits |= (lemire_value(st.next(), 2u) & 1u) << e;
     }
     a.sgn[w] = bits;
@@ -687,9 +688,22 @@ int srht_fused_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int6
   return 1;
 }
 
-int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const adask_pcg64* g,
-               uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out, int64_t ldo, double c1,
-               double c2, int accumulate, cudaStream_t st) {
+namespace {
+// one (sub-)block of n_pad padded rows: its rows of A, valid row count, first
+// sign draw, sign scratch and output
+struct FusedSub {
+  const void* A;
+  int64_t n;
+  uint64_t draw0;
+  uint32_t* sgn;
+  void* out;
+};
+
+// The selected rows idx (within a block of n_pad rows) of every sub-block in
+// `subs`, with one host plan and one launch per sub-block.
+int srht_fused_subs(adask_ctx* ctx, int dtype, const FusedSub* subs, int nsub, int64_t d, int64_t lda,
+                    const adask_pcg64* g, int64_t n_pad, const int64_t* idx, int64_t m, int64_t ldo, double c1,
+                    double c2, int accumulate, cudaStream_t st) {
   const int L = ilog2f(n_pad);
   const int L2 = L - kB1;
   const int64_t G = n_pad >> kB1;
@@ -777,14 +791,11 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
   unsigned* sync = (unsigned*)sw;
 
   CUtensorMap am, zm;
-  ADASK_TRY(tensor_map_rows3d(&am, dtype, A, n, d, lda, (uint32_t)W, kQ, 32u));
   ADASK_TRY(tensor_map_rows3d(&zm, dtype, zw, (int64_t)npanels * zrows, W, W, (uint32_t)W, kQ, 32u));
 
   FusedArgs a{};
-  a.n_valid = n;
   a.dbytes = dbytes;
   a.gen = GenState::from(*g);
-  a.sgn = sgn;
   a.nwords = n_pad / 32;
   a.lo2slot = (const int32_t*)pw;
   a.toff = (const int32_t*)pw + o_toff;
@@ -793,12 +804,10 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
   a.Z = (unsigned char*)zw;
   a.zrows = zrows;
   a.G = G;
-  a.out = (unsigned char*)out;
   a.ldo_b = ldo * (int64_t)esz;
   a.c1 = c1;
   a.c2 = c2;
   a.accumulate = accumulate;
-  a.vec_out = ((uintptr_t)out % 8 == 0) && (a.ldo_b % 8 == 0);
   a.gp = gp;
   a.npanels = npanels;
   a.n_items = n_items;
@@ -814,8 +823,21 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
     ADASK_CUDA(cudaMemsetAsync(a.tlog, 0, tl_n * 8, st));
   }
 #endif
-  const int rc = dtype == ADASK_F64 ? launch_fused<double>(ctx, L2, am, zm, a, st)
-                                    : launch_fused<float>(ctx, L2, am, zm, a, st);
+  int rc = ADASK_OK;
+  for (int sb = 0; sb < nsub && rc == ADASK_OK; ++sb) {
+    const FusedSub& u = subs[sb];
+    if (u.n <= 0) {  // all padding: zero rows (0 / c1 * c2 = 0)
+      if (!accumulate) ADASK_CUDA(cudaMemset2DAsync(u.out, (size_t)ldo * esz, 0, (size_t)dbytes, (size_t)m, st));
+      continue;
+    }
+    ADASK_TRY(tensor_map_rows3d(&am, dtype, u.A, u.n, d, lda, (uint32_t)W, kQ, 32u));
+    a.n_valid = u.n;
+    a.draw0 = u.draw0;
+    a.sgn = u.sgn;
+    a.out = (unsigned char*)u.out;
+    a.vec_out = ((uintptr_t)u.out % 8 == 0) && (a.ldo_b % 8 == 0);
+    rc = dtype == ADASK_F64 ? launch_fused<double>(ctx, L2, am, zm, a, st) : launch_fused<float>(ctx, L2, am, zm, a, st);
+  }
 #ifdef FUSED_TRACE
   if (tr && rc == ADASK_OK) {
     std::vector<unsigned long long> h(tl_n);
@@ -829,6 +851,131 @@ int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, i
   }
 #endif
   return rc;
+}
+
+// combine the S = 2^LS sub-block partials of every selected row: stages
+// 18 .. 18 + LS - 1 of the butterfly DAG (lower + upper / lower - upper by the
+// row's bit), then the reference's two scaling steps
+template <typename T, int LS>
+__global__ void k_srht_combine(const T* __restrict__ P, int64_t mu, int64_t d, const int32_t* __restrict__ urow,
+                               const int32_t* __restrict__ uhi, int64_t m, T* __restrict__ out, int64_t ldo,
+                               double c1, double c2, int accumulate) {
+  constexpr int S = 1 << LS;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * d) return;
+  const int64_t k = e / d, j = e - k * d;
+  const int hi = uhi[k];
+  const T* p = P + (int64_t)urow[k] * d + j;
+  T v[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) v[s] = p[(int64_t)s * mu * d];
+#pragma unroll
+  for (int b = 0; b < LS; ++b) {
+    const bool up = (hi >> b) & 1;
+#pragma unroll
+    for (int s = 0; s < (S >> (b + 1)); ++s) {
+      const T x0 = v[2 * s], x1 = v[2 * s + 1];
+      if constexpr (sizeof(T) == 8)
+        v[s] = up ? __dsub_rn(x0, x1) : __dadd_rn(x0, x1);
+      else
+        v[s] = up ? __fsub_rn(x0, x1) : __fadd_rn(x0, x1);
+    }
+  }
+  T y;
+  if constexpr (sizeof(T) == 8)
+    y = dscale(v[0], c1, c2);
+  else
+    y = fscale(v[0], c1, c2);
+  T* o = out + k * ldo + j;
+  *o = accumulate ? (T)(*o + y) : y;
+}
+
+}  // namespace
+
+int srht_fused(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const adask_pcg64* g,
+               uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out, int64_t ldo, double c1,
+               double c2, int accumulate, cudaStream_t st) {
+  const FusedSub one{A, n, 0, sgn, out};
+  return srht_fused_subs(ctx, dtype, &one, 1, d, lda, g, n_pad, idx, m, ldo, c1, c2, accumulate, st);
+}
+
+// Blocks of 2^19 .. 2^22 padded rows: the transform's first 18 stages act
+// inside aligned sub-blocks of 2^18 rows, so each sub-block runs the fused
+// kernel (Z stays L2-resident) for the DISTINCT low 18-bit values of the
+// selected rows, unscaled, into a partial buffer; k_srht_combine applies the
+// remaining stages for every selected row.  HBM traffic: A once plus the
+// partials (S mu d) instead of A plus a Z round trip.
+int srht_fused_big_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, int64_t lda, int64_t m) {
+  const char* env = getenv("ADASK_SRHT_FUSED");
+  if ((env && atoi(env) == 0) || getenv("ADASK_FWHT_PIPE")) return 0;
+  if (kB1 != 9) return 0;
+  const int L = ilog2f(n_pad);
+  if (L < 19 || L > 22) return 0;
+  static const int64_t min_m = getenv("ADASK_SRHT_BIG_MIN_M") ? atoll(getenv("ADASK_SRHT_BIG_MIN_M")) : 0;
+  if (m < min_m || m >= (1 << 20)) return 0;
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  if (((uintptr_t)A & 15) || ((size_t)lda * esz) % 16 || n % 32) return 0;
+  return 1;
+}
+
+int srht_fused_big(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                   const adask_pcg64* g, uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out,
+                   int64_t ldo, double c1, double c2, int accumulate, cudaStream_t st) {
+  constexpr int kSubL = 18;
+  constexpr int64_t kSub = 1ll << kSubL;
+  const int LS = ilog2f(n_pad) - kSubL;
+  const int S = 1 << LS;
+  const size_t esz = dtype == ADASK_F64 ? 8 : 4;
+  // distinct low parts (sorted) and, per selected row, its partial row and high bits
+  std::vector<int64_t> lo((size_t)m);
+  for (int64_t k = 0; k < m; ++k) lo[(size_t)k] = idx[k] & (kSub - 1);
+  std::vector<int64_t> u(lo);
+  std::sort(u.begin(), u.end());
+  u.erase(std::unique(u.begin(), u.end()), u.end());
+  const int64_t mu = (int64_t)u.size();
+  std::vector<int32_t> map((size_t)(2 * m));
+  for (int64_t k = 0; k < m; ++k) {
+    map[(size_t)k] = (int32_t)(std::lower_bound(u.begin(), u.end(), lo[(size_t)k]) - u.begin());
+    map[(size_t)(m + k)] = (int32_t)(idx[k] >> kSubL);
+  }
+  void* pw = nullptr;
+  ADASK_TRY(ctx->ws[WS_SRHT_PART].get((size_t)S * mu * d * esz, st, &pw));
+  void* mw = nullptr;
+  ADASK_TRY(ctx->ws[WS_SRHT_MAP].get(map.size() * 4, st, &mw));
+  ADASK_TRY(upload_async(ctx, mw, map.data(), map.size() * 4, st));
+  std::vector<FusedSub> subs((size_t)S);
+  for (int sb = 0; sb < S; ++sb) {
+    FusedSub& f = subs[(size_t)sb];
+    f.A = (const char*)A + (size_t)sb * kSub * lda * esz;
+    f.n = std::max<int64_t>(0, std::min<int64_t>(kSub, n - sb * kSub));
+    f.draw0 = (uint64_t)sb * kSub;
+    f.sgn = sgn + (size_t)sb * (kSub / 32);
+    f.out = (char*)pw + (size_t)sb * mu * d * esz;
+  }
+  ADASK_TRY(srht_fused_subs(ctx, dtype, subs.data(), S, d, lda, g, kSub, u.data(), mu, d, 1.0, 0.0, 0, st));
+  const unsigned blocks = (unsigned)cdiv(m * d, 256);
+  const int32_t* urow = (const int32_t*)mw;
+  const int32_t* uhi = urow + m;
+#define COMB(T, LSV)                                                                                            \
+  k_srht_combine<T, LSV><<<blocks, 256, 0, st>>>((const T*)pw, mu, d, urow, uhi, m, (T*)out, ldo, c1, c2, accumulate)
+  if (dtype == ADASK_F64) {
+    switch (LS) {
+      case 1: COMB(double, 1); break;
+      case 2: COMB(double, 2); break;
+      case 3: COMB(double, 3); break;
+      default: COMB(double, 4); break;
+    }
+  } else {
+    switch (LS) {
+      case 1: COMB(float, 1); break;
+      case 2: COMB(float, 2); break;
+      case 3: COMB(float, 3); break;
+      default: COMB(float, 4); break;
+    }
+  }
+#undef COMB
+  ADASK_LAUNCHED(ctx);
+  return ADASK_OK;
 }
 
 }  // namespace adask

@@ -101,3 +101,35 @@ def test_fused_srht_accumulate(ak, dtype, monkeypatch):
     o2 = base.clone()
     srht_dev(A, 900, 21, out=o2, accumulate=True)
     assert torch.equal(o1, o2)
+
+
+# ---- blocks of 2^19 .. 2^22 padded rows: the fused kernel per 2^18-row
+# sub-block + the combine of the partials (srht_fused_big)
+@pytest.mark.parametrize("n,d,m,seed", [
+    (1 << 19, 6, 300, 1),               # two sub-blocks
+    ((1 << 19) + 32, 5, 2000, 2),       # 2^20 padded: sub-block 2 has 32 rows, sub-block 3 none
+    ((1 << 20) - 4096, 4, 70000, 3),    # four sub-blocks, repeated low parts, ragged tail
+    (1 << 21, 2, 64, 4),                # config-4 block length, eight sub-blocks
+])
+def test_fused_srht_big_blocks_bitwise(ak, n, d, m, seed, monkeypatch):
+    _fused(monkeypatch)
+    A = np.random.default_rng(seed).standard_normal((n, d))
+    got = ak.sketch_srht(A, m, seed).SA
+    assert np.array_equal(got, O.sketch_srht(A, m, seed))
+
+
+@pytest.mark.parametrize("n,d,m,acc", [(1 << 19, 24, 1000, False), ((1 << 20) + 64, 9, 5000, True),
+                                       (1 << 22, 4, 300, False)])
+def test_fused_srht_big_blocks_fp32_match_two_launch(ak, n, d, m, acc, monkeypatch):
+    """fp32, incl. accumulation into an existing sketch (the block SRHT of
+    config 4 adds its blocks' sketches) and sixteen sub-blocks: bitwise the
+    two-launch pipeline's result."""
+    from paper_2104_14101_b200.embeddings import srht_dev
+
+    A = torch.randn(n, d, dtype=torch.float32, device="cuda", generator=torch.Generator("cuda").manual_seed(n + m))
+    base = torch.randn(m, d, dtype=torch.float32, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+    _fused(monkeypatch)
+    got = srht_dev(A, m, 5, out=base.clone(), accumulate=True) if acc else srht_dev(A, m, 5)
+    monkeypatch.setenv("ADASK_SRHT_FUSED", "0")
+    ref = srht_dev(A, m, 5, out=base.clone(), accumulate=True) if acc else srht_dev(A, m, 5)
+    assert torch.equal(got, ref)
