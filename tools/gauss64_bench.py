@@ -9,6 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2104_14101_b200.embeddings import gaussian_dev  # noqa: E402
 
 shapes = [(4096, 256, 256), (65536, 1024, 256), (65536, 1024, 1024), (1 << 18, 512, 2048)]
+if os.environ.get("SHAPES"):
+    shapes = [shapes[int(i)] for i in os.environ["SHAPES"].split(",")]
 for n, d, m in shapes:
     A = torch.randn((n, d), dtype=torch.float64, device="cuda")
     for _ in range(2):

@@ -16,3 +16,5 @@ ncu --set full --clock-control none --import-source on -k regex:k_gram_dmma -s 2
 echo "gram rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:k_chol_df -s 6 -c 1 -o gpurun_out/r02_chol -f $CMD > gpurun_out/ncu_chol.log 2>&1
 echo "chol rc=$?"
+SHAPES=2 python tools/gauss64_bench.py > /dev/null 2>&1 && SHAPES=2 ncu --set full --clock-control none --import-source on -k regex:k_gemm_tn_dmma -s 2 -c 1 -o gpurun_out/r02_gauss64 -f python tools/gauss64_bench.py > gpurun_out/ncu_gauss64.log 2>&1
+echo "gauss64 rc=$?"
