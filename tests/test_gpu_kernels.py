@@ -342,3 +342,19 @@ def test_gaussian_rows_offset_matches_oracle(k0, mk, m_total, dtype, tf32):
         assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
     else:
         assert np.all(np.abs(got - ref) <= 2.0**-9 * (np.abs(S) @ np.abs(Aref)) + 1e-5)
+
+
+def test_repeated_mixed_launches_stress():
+    """Ten seconds of random-size dataflow Cholesky factorizations (fp64 /
+    fp32, flag epochs and ticket bases carried across launches) interleaved
+    with fused SRHT sketches (self-resetting counters, publisher mailboxes),
+    each checked against numpy / the oracle (tools/stress_r02.py)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SECONDS="10", SEED="3")
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "stress_r02.py")], env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0 and "stress ok" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
