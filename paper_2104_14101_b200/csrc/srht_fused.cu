@@ -912,7 +912,8 @@ int srht_fused_big_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, 
   const int L = ilog2f(n_pad);
   if (L < 19 || L > 22) return 0;
   static const int64_t min_m = getenv("ADASK_SRHT_BIG_MIN_M") ? atoll(getenv("ADASK_SRHT_BIG_MIN_M")) : 0;
-  if (m < min_m || m >= (1 << 20)) return 0;
+  // the partial rows (S mu d, mu <= m) stay under half of the block's own bytes
+  if (m < min_m || m > (1 << 17)) return 0;
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
   if (((uintptr_t)A & 15) || ((size_t)lda * esz) % 16 || n % 32) return 0;
   return 1;
