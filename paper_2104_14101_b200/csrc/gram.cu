@@ -16,7 +16,8 @@
 // fp64 at the fragment load, so the fp32 Grams accumulate in fp64.
 //
 // Kernel: 256 threads (8 warps as 2 x 4, warp tile 64 x 32 = 4 x 4
-// m16n8k4 MMAs), 4-stage cp.async pipeline of 128-byte-deep operand tiles
+// m16n8k4 MMAs), cp.async pipeline (3 stages of 256-byte-deep operand tiles
+// on the K-outer side, 4 stages of 128-byte-deep ones on the K-contiguous side)
 // with padded pitches that make every fragment load (LDS.128 for fp64,
 // LDS.64 for fp32) bank-conflict free, and a fragment-to-C index permutation
 // that lets one 16-byte load feed two MMA rows (K-outer) or two k steps
@@ -25,17 +26,24 @@
 #include "common.cuh"
 #include "gemm.cuh"
 
+// bytes of reduction depth per pipeline stage of the K-outer kernels: 256 with
+// three stages measured 2-3% faster than 128 with four (one CTA barrier per
+// 32 instead of 16 fp64 reduction steps); the K-contiguous side stays at 128
+#ifndef GRAM_KO_DEPTH
+#define GRAM_KO_DEPTH 256
+#endif
 namespace adask {
 namespace gram {
 
 constexpr int BT = 128;     // C tile edge
 constexpr int NT = 256;     // threads: 8 warps, 2 (rows) x 4 (cols)
-constexpr int STAGES = 4;
 
 template <typename T, bool KC>
 struct Lay {
   static constexpr int ES = (int)sizeof(T);
-  static constexpr int BK = 128 / ES;   // reduction depth per stage (128 bytes)
+  // reduction depth per stage: 128 bytes (K-contiguous), GRAM_KO_DEPTH bytes (K-outer)
+  static constexpr int BK = (KC ? 128 : GRAM_KO_DEPTH) / ES;
+  static constexpr int NSTAGE = (!KC && GRAM_KO_DEPTH > 128) ? 3 : 4;
   static constexpr int V = 16 / ES;     // elements per 16-byte chunk
   // K-outer: [BK][PITCH] (rows = reduction index, 128 C indices per row);
   // K-contiguous: [BT][PITCH] (rows = C index, BK reduction values per row)
@@ -44,7 +52,8 @@ struct Lay {
   static constexpr int ROWS = KC ? BT : BK;
   static constexpr int OP_BYTES = ROWS * PITCH_B;
   static constexpr int STAGE_BYTES = 2 * OP_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES;
+  static constexpr int SMEM = NSTAGE * STAGE_BYTES;
+  static constexpr int NQ = ROWS * (KC ? BK : BT) / V / 256;  // 16-byte chunks per thread and operand tile
 };
 
 struct Args {
@@ -105,8 +114,8 @@ __device__ __forceinline__ void load_tile(const void* Xv, int64_t ld, int64_t N,
   using Lt = Lay<T, KC>;
   const T* X = reinterpret_cast<const T*>(Xv);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int c = threadIdx.x + NT * q;  // chunk 0..1023
+  for (int q = 0; q < Lt::NQ; ++q) {
+    const int c = threadIdx.x + NT * q;  // chunk index within the operand tile
     int r, cc;
     int64_t grow, gcol;
     int bytes;
@@ -168,20 +177,20 @@ __global__ void __launch_bounds__(NT, 1) k_gram_dmma(Args a) {
   };
 
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < Lt::NSTAGE - 1; ++s) {
     if (s < nst) issue(s, s);
     cp_commit();
   }
   for (int it = 0; it < nst; ++it) {
-    cp_wait<STAGES - 2>();
+    cp_wait<Lt::NSTAGE - 2>();
     __syncthreads();
     {
-      const int nx = it + STAGES - 1;
-      if (nx < nst) issue(nx % STAGES, nx);
+      const int nx = it + Lt::NSTAGE - 1;
+      if (nx < nst) issue(nx % Lt::NSTAGE, nx);
       cp_commit();
     }
     if (!active) continue;
-    const unsigned char* sb = smem + (it % STAGES) * Lt::STAGE_BYTES;
+    const unsigned char* sb = smem + (it % Lt::NSTAGE) * Lt::STAGE_BYTES;
     const T* As = reinterpret_cast<const T*>(sb);
     const T* Bs = reinterpret_cast<const T*>(diag ? sb : sb + Lt::OP_BYTES);
     if constexpr (!KC) {
@@ -400,20 +409,20 @@ __global__ void __launch_bounds__(NT, 1) k_gemm_tn_dmma(RArgs a) {
     load_tile<T, false>(a.Y, a.ldy, a.N, sb + Lt::OP_BYTES, cj, k0, kend);
   };
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < Lt::NSTAGE - 1; ++s) {
     if (s < nst) issue(s, s);
     cp_commit();
   }
   for (int it = 0; it < nst; ++it) {
-    cp_wait<STAGES - 2>();
+    cp_wait<Lt::NSTAGE - 2>();
     __syncthreads();
     {
-      const int nx = it + STAGES - 1;
-      if (nx < nst) issue(nx % STAGES, nx);
+      const int nx = it + Lt::NSTAGE - 1;
+      if (nx < nst) issue(nx % Lt::NSTAGE, nx);
       cp_commit();
     }
     if (!active) continue;
-    const unsigned char* sb = smem + (it % STAGES) * Lt::STAGE_BYTES;
+    const unsigned char* sb = smem + (it % Lt::NSTAGE) * Lt::STAGE_BYTES;
     const T* As = reinterpret_cast<const T*>(sb);
     const T* Bs = reinterpret_cast<const T*>(sb + Lt::OP_BYTES);
 #pragma unroll
