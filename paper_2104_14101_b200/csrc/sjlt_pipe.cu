@@ -189,14 +189,19 @@ int sjlt_accumulate_pipe(adask_ctx* ctx, int dtype, const void* A, int64_t d, in
   // panel: the whole row up to 16 KB; narrower (>= 4 KB) until there are
   // >= 2 items per SM
   const int64_t row_bytes = (int64_t)d * esz;
+  // Whole 16 KB rows stream fastest (measured at 2^20 x 2048 fp64, m = 128:
+  // 2.66 ms with 16 KB pieces, 3.46 with 8 KB, 5.1 with 4 KB: the DRAM sees
+  // short random pieces) and a partly filled second wave costs little (the
+  // active CTAs get the idle ones' bandwidth; m = 256: 2.81 ms with 256 items
+  // against 3.53 with 512 half-row items), so the panel is halved only while
+  // fewer than ~2/3 of the SMs would have an item.
   int64_t pb = std::min<int64_t>(row_bytes, (int64_t)kMaxChunks * kNW * 32 * 16);
-  const int64_t min_pb = getenv("ADASK_SJLT_MINPB") ? atoll(getenv("ADASK_SJLT_MINPB")) : 4096;
-  while (pb > min_pb && m * cdiv(row_bytes, pb) < 2 * kNumSMs) pb /= 2;
+  const int64_t min_pb = getenv("ADASK_SJLT_MINPB") ? atoll(getenv("ADASK_SJLT_MINPB")) : 2048;
+  while (pb > min_pb && m * cdiv(row_bytes, pb) < 96) pb /= 2;
   pb = std::max<int64_t>(16, pb / 16 * 16);
-  // few long buckets (m < 256): the items cannot be balanced over the SMs
-  // (each bucket is one sequential chain) -- the register kernel's narrow mode
-  // is faster there (measured at 2^20 x 2048 fp64: m = 64, 128)
-  if (mode == 1 && m < 256) return ADASK_OK;
+  // very few buckets: the register kernel's narrow mode (ADASK_SJLT_PIPE=2 forces this one)
+  static const int64_t pipe_min_m = getenv("ADASK_SJLT_PIPE_MIN_M") ? atoll(getenv("ADASK_SJLT_PIPE_MIN_M")) : 16;
+  if (mode == 1 && m < pipe_min_m) return ADASK_OK;
   SjltPipeArgs a{};
   a.A = A;
   a.lda = lda;
