@@ -726,9 +726,13 @@ int srht_fused_subs(adask_ctx* ctx, int dtype, const FusedSub* subs, int nsub, i
   const int64_t dbytes = d * (int64_t)esz;
   const int npanels = (int)cdiv(dbytes, kRowB);
   const int64_t zbudget = (getenv("ADASK_SRHT_FUSED_ZMB") ? atoll(getenv("ADASK_SRHT_FUSED_ZMB")) : 24) << 20;
-  const int lag = std::max(1, getenv("ADASK_SRHT_FUSED_LAG") ? atoi(getenv("ADASK_SRHT_FUSED_LAG")) : 2);
   const int64_t zpanel = zrows * kRowB;
   const int gp = (int)std::max<int64_t>(1, std::min<int64_t>(npanels, zbudget / zpanel));
+  // pass 2 trails pass 1 by `lag` groups, so lag + 1 groups of Z are live: two
+  // groups of lag while that stays within ~80 MB of the 126 MB L2, else one
+  // (2^18-row sub-blocks have 32 MB panels: lag 2 -> 1 is 568 -> 484 us at m = 4096)
+  const int lag = getenv("ADASK_SRHT_FUSED_LAG") ? std::max(1, atoi(getenv("ADASK_SRHT_FUSED_LAG")))
+                                                 : (3 * gp * zpanel <= (80ll << 20) ? 2 : 1);
   const int ng = (int)cdiv(npanels, gp);
   // work list: P1(0..lag-1), then [P1(g) P2(g-lag)] ..., then the last P2s
   std::vector<int4> segs;
