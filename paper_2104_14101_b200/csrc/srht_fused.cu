@@ -926,8 +926,9 @@ int srht_fused_big_eligible(int dtype, const void* A, int64_t n, int64_t n_pad, 
 int srht_fused_big(adask_ctx* ctx, int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
                    const adask_pcg64* g, uint32_t* sgn, int64_t n_pad, const int64_t* idx, int64_t m, void* out,
                    int64_t ldo, double c1, double c2, int accumulate, cudaStream_t st) {
-  constexpr int kSubL = 18;
-  constexpr int64_t kSub = 1ll << kSubL;
+  static const int sub_env = getenv("ADASK_SRHT_BIG_SUBL") ? atoi(getenv("ADASK_SRHT_BIG_SUBL")) : 18;
+  const int kSubL = std::min(18, std::max({sub_env, ilog2f(n_pad) - 4, 11}));
+  const int64_t kSub = 1ll << kSubL;
   const int LS = ilog2f(n_pad) - kSubL;
   const int S = 1 << LS;
   const size_t esz = dtype == ADASK_F64 ? 8 : 4;
